@@ -1,0 +1,162 @@
+"""fp64 CPU oracle for the DCNv4 spatial aggregation -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg
+and ``--impl reference``) may import this package.  The product path
+(``paper_2401_06197_b200``) never imports it, and this package imports nothing from
+the product path: the two share no code.
+
+The arithmetic lives in ``dcnv4_oracle.c`` (plain C, fp64, OpenMP over (n, g)); this
+module only builds it with gcc, marshals numpy arrays, and converts stored values
+exactly to fp64.  Every function cites the passage it follows:
+
+* forward  -- PAPER.md Eq. (1)-(2), softmax removed;
+* backward -- Eq. (1) differentiated, right derivative at kinks;
+* softmax  -- the DCNv3 normalisation over K, behind ``softmax=True``.
+
+Parity status: every output is pinned (tests/test_oracle_pins.py); see DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dcnv4_oracle.c")
+_LIB = os.path.join(_HERE, "libdcnv4_oracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (fp64, no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+             "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        lib.oracle_output_size.argtypes = [P, P, P]
+        lib.oracle_forward.argtypes = [P, ctypes.c_double, P, P, P, P]
+        lib.oracle_backward.argtypes = [P, ctypes.c_double, P, P, P, P, P, P, P]
+        lib.oracle_forward.restype = ctypes.c_int
+        lib.oracle_backward.restype = ctypes.c_int
+        lib.oracle_output_size.restype = ctypes.c_int
+        lib.oracle_geom_len.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+@dataclass(frozen=True)
+class Geometry:
+    """Problem geometry (Eq. (1): x in R^{HxWxC}, G groups, K = kh*kw points).
+
+    ``om_stride`` is S, the channel count of one offset_mask row (0 -> 3*G*K)."""
+    N: int
+    H: int
+    W: int
+    G: int
+    D: int
+    kh: int = 3
+    kw: int = 3
+    sh: int = 1
+    sw: int = 1
+    ph: int = 1
+    pw: int = 1
+    dh: int = 1
+    dw: int = 1
+    offset_scale: float = 1.0
+    om_stride: int = 0
+    softmax: bool = False
+
+    @property
+    def K(self) -> int:
+        return self.kh * self.kw
+
+    @property
+    def C(self) -> int:
+        return self.G * self.D
+
+    @property
+    def S(self) -> int:
+        return self.om_stride if self.om_stride else 3 * self.G * self.K
+
+    def out_hw(self):
+        # conv2d output arithmetic (reading R4, "as in regular convolutions")
+        Ho = (self.H + 2 * self.ph - self.dh * (self.kh - 1) - 1) // self.sh + 1
+        Wo = (self.W + 2 * self.pw - self.dw * (self.kw - 1) - 1) // self.sw + 1
+        return Ho, Wo
+
+    def vec(self) -> np.ndarray:
+        return np.array([self.N, self.H, self.W, self.G, self.D, self.kh, self.kw, self.sh,
+                         self.sw, self.ph, self.pw, self.dh, self.dw, self.S,
+                         int(self.softmax)], dtype=np.int64)
+
+
+def _f64(a) -> np.ndarray:
+    """Exact conversion of stored fp32/fp16/bf16 values to a contiguous fp64 array."""
+    if hasattr(a, "detach"):  # torch tensor: .double() is exact for fp32/fp16/bf16
+        a = a.detach().to("cpu").double().numpy()
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def forward(geom: Geometry, x, om, with_abs: bool = False):
+    """y = DCNv4(x, offset_mask) in fp64 (Eq. (1)-(2)).  Returns y or (y, y_abs)."""
+    lib = _load()
+    Ho, Wo = geom.out_hw()
+    x = _f64(x).reshape(geom.N, geom.H, geom.W, geom.C)
+    om = _f64(om).reshape(geom.N, Ho, Wo, geom.S)
+    y = np.empty((geom.N, Ho, Wo, geom.C), np.float64)
+    ya = np.empty_like(y) if with_abs else None
+    gv = geom.vec()
+    rc = lib.oracle_forward(_ptr(gv), geom.offset_scale, _ptr(x), _ptr(om), _ptr(y),
+                            _ptr(ya) if with_abs else None)
+    if rc:
+        raise ValueError(f"oracle_forward failed with code {rc}")
+    return (y, ya) if with_abs else y
+
+
+def backward(geom: Geometry, x, om, gy, with_abs: bool = False):
+    """(grad_x, grad_om) of Eq. (1) in fp64; with_abs adds their magnitude scales."""
+    lib = _load()
+    Ho, Wo = geom.out_hw()
+    x = _f64(x).reshape(geom.N, geom.H, geom.W, geom.C)
+    om = _f64(om).reshape(geom.N, Ho, Wo, geom.S)
+    gy = _f64(gy).reshape(geom.N, Ho, Wo, geom.C)
+    gx = np.empty_like(x)
+    gom = np.empty_like(om)
+    gxa = np.empty_like(x) if with_abs else None
+    goma = np.empty_like(om) if with_abs else None
+    gv = geom.vec()
+    rc = lib.oracle_backward(_ptr(gv), geom.offset_scale, _ptr(x), _ptr(om), _ptr(gy),
+                             _ptr(gx), _ptr(gom), _ptr(gxa) if with_abs else None,
+                             _ptr(goma) if with_abs else None)
+    if rc:
+        raise ValueError(f"oracle_backward failed with code {rc}")
+    return (gx, gom, gxa, goma) if with_abs else (gx, gom)
+
+
+def abs_scaled_error(gpu, ref, scale) -> float:
+    """max_i |gpu_i - ref_i| / (A_i + 1e-30 * max A)  (SURVEY 8(c).4 metric)."""
+    gpu = _f64(gpu)
+    ref = _f64(ref)
+    scale = _f64(scale)
+    den = scale + 1e-30 * max(float(scale.max(initial=0.0)), 1e-300)
+    if gpu.size == 0:
+        return 0.0
+    return float((np.abs(gpu - ref) / den).max())

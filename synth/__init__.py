@@ -1,0 +1,83 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and bench.py.
+
+This module holds NONE of the method's arithmetic: it only draws random numbers of the
+shapes, ranges and structure of the paper's workloads (DESIGN.md "Input recipe",
+SURVEY.md 8(d).1).  Both the oracle side and the CUDA side receive the same tensors.
+
+Recipe (per image n, global index ``n`` so 1/2/4/8-rank shards see identical images):
+  seed(tensor_id, n) = 20240111 + 1000 * tensor_id + n   (tensor_id: x=0, om=1, gy=2)
+  x  ~ U(-1, 1)                      input feature map, NHWC  [N, H, W, G*D]
+  dx, dy ~ U(-2, 2) i.i.d.           offsets (SPEC S:133 seeded case), in offset_mask
+  m  ~ U(-1, 1)                      unnormalised modulation ("unbounded")
+  padding channels of offset_mask (S > 3GK) ~ U(-1, 1) (must be ignored)
+  gy ~ U(-1, 1)                      upstream gradient, NHWC [N, Ho, Wo, G*D]
+Values are drawn in fp32 with torch's CPU generator and then cast (RN-even) to the
+storage dtype; the oracle is fed the same quantised values.
+Offset variants: "u2" (default), "zero", "u8" (weak locality), "smooth" (coarse 8x8
+U(-2,2) field upsampled bilinearly, mimicking learned offsets).
+"""
+from __future__ import annotations
+
+import torch
+
+SEED_BASE = 20240111
+TENSOR_X, TENSOR_OM, TENSOR_GY = 0, 1, 2
+
+DTYPES = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+
+
+def seed_of(tensor_id: int, image: int) -> int:
+    return SEED_BASE + 1000 * tensor_id + image
+
+
+def _uniform(shape, seed, lo, hi):
+    g = torch.Generator().manual_seed(seed)
+    return torch.rand(shape, generator=g, dtype=torch.float32) * (hi - lo) + lo
+
+
+def image_x(H, W, C, image):
+    return _uniform((H, W, C), seed_of(TENSOR_X, image), -1.0, 1.0)
+
+
+def image_gy(Ho, Wo, C, image):
+    return _uniform((Ho, Wo, C), seed_of(TENSOR_GY, image), -1.0, 1.0)
+
+
+def image_om(Ho, Wo, G, K, S, image, offsets="u2"):
+    """One image's fused offset_mask row block [Ho, Wo, S] (layout: DESIGN.md R3)."""
+    g = torch.Generator().manual_seed(seed_of(TENSOR_OM, image))
+    om = torch.rand((Ho, Wo, S), generator=g, dtype=torch.float32) * 2.0 - 1.0  # m, pad
+    off = torch.rand((Ho, Wo, G, 2 * K), generator=g, dtype=torch.float32)
+    if offsets == "u2":
+        off = off * 4.0 - 2.0
+    elif offsets == "u8":
+        off = off * 16.0 - 8.0
+    elif offsets == "zero":
+        off = torch.zeros_like(off)
+    elif offsets == "smooth":
+        coarse = torch.rand((1, G * 2 * K, 8, 8), generator=g) * 4.0 - 2.0
+        up = torch.nn.functional.interpolate(coarse, size=(Ho, Wo), mode="bilinear",
+                                             align_corners=True)
+        off = up[0].permute(1, 2, 0).reshape(Ho, Wo, G, 2 * K)
+    else:
+        raise ValueError(f"unknown offset distribution {offsets!r}")
+    for grp in range(G):
+        om[:, :, grp * 3 * K: grp * 3 * K + 2 * K] = off[:, :, grp]
+    return om
+
+
+def make_case(N, H, W, G, D, Ho, Wo, K, S, dtype="f32", images=None, offsets="u2",
+              with_gy=True):
+    """CPU tensors (x, om, gy) for images ``images`` (default range(N)) in ``dtype``."""
+    images = list(range(N)) if images is None else list(images)
+    C = G * D
+    dt = DTYPES[dtype]
+    x = torch.stack([image_x(H, W, C, n) for n in images]).to(dt) if images else \
+        torch.empty((0, H, W, C), dtype=dt)
+    om = torch.stack([image_om(Ho, Wo, G, K, S, n, offsets) for n in images]).to(dt) \
+        if images else torch.empty((0, Ho, Wo, S), dtype=dt)
+    gy = None
+    if with_gy:
+        gy = torch.stack([image_gy(Ho, Wo, C, n) for n in images]).to(dt) if images else \
+            torch.empty((0, Ho, Wo, C), dtype=dt)
+    return x, om, gy
