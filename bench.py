@@ -1,0 +1,543 @@
+#!/usr/bin/env python
+"""bench.py -- DCNv4 spatial aggregation on B200: the driver's benchmark contract.
+
+Default workload (BASELINE.json configs[3], "c4"): one training step of the DCNv4 core
+operator over the four InternImage-T 224^2 stage shapes (56^2x64 G4, 28^2x128 G8,
+14^2x256 G16, 7^2x512 G32; D=16), fp32, forward + backward (every SURVEY.md 8(a) row),
+global batch 512 sharded by batch over the ranks (strong scaling, no collective on the
+data path).  Inputs are seeded synthetic tensors (synth/)
+resident in HBM; the per-rank working set (>= 0.9 GB at 8 ranks) exceeds the 126 MB L2,
+so no flush is needed between timed steps.
+
+Timed region: K steps captured in ONE CUDA graph with external event nodes between the
+library calls, replayed once between a barrier + synchronize on both sides; the step time
+is the max over ranks.  Per-call durations come from those event nodes (on the launching
+stream), giving the per-stage table and the roofline of the dominant kernel.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2_f32|c2_f16|c3_f16|c5_bf16]
+  python bench.py --impl reference ...   # the fp64 CPU oracle as the reference arm
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# OpenMP of the oracle (cpu_baseline / reference arm) reads this at library load.
+os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+
+METRIC = ("DCNv4 fwd/bwd µs and HBM GB/s (% of B200 peak) per stage shape; "
+          "imgs/s at 1/2/4/8 GPU")
+STAGES_224 = [(56, 56, 4), (28, 28, 8), (14, 14, 16), (7, 7, 32)]
+STAGES_800 = [(200, 320, 4), (100, 160, 8), (50, 80, 16), (25, 40, 32)]
+STAGES_UNET = [(64, 64, 20), (32, 32, 40), (16, 16, 80)]
+WORKLOADS = {
+    "c4": dict(desc="BASELINE configs[3]: training fwd+bwd, InternImage-T 224^2 four-stage "
+                    "shapes, D=16, fp32, global batch 512 sharded by batch",
+               stages=STAGES_224, dtype="f32", batch=512, backward=True, shard=True),
+    "c2_f32": dict(desc="BASELINE configs[1]: 224^2 stage sweep, D=16, fp32 forward, batch 64",
+                   stages=STAGES_224, dtype="f32", batch=64, backward=False, shard=False),
+    "c2_f16": dict(desc="BASELINE configs[1]: 224^2 stage sweep, D=16, fp16 forward, batch 64",
+                   stages=STAGES_224, dtype="f16", batch=64, backward=False, shard=False),
+    "c3_f16": dict(desc="BASELINE configs[2]: 800x1280 FlashInternImage stages, D=16, fp16 "
+                        "forward, batch 8", stages=STAGES_800, dtype="f16", batch=8,
+                   backward=False, shard=False),
+    "c5_bf16": dict(desc="BASELINE configs[4]: U-Net 64^2 latents C=320/640/1280, D=16, bf16 "
+                         "fwd+bwd, batch 32", stages=STAGES_UNET, dtype="bf16", batch=32,
+                    backward=True, shard=False),
+}
+D = 16
+K = 9
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    FIELDS = ("uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid: str | None):
+        self.uuid = uuid
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            if self.uuid and parts[0] != self.uuid:
+                continue
+            self.samples.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        inside = [s for t, s in self.samples if t0 <= t <= t1]
+        use = inside or [min(self.samples, key=lambda ts: abs(ts[0] - (t0 + t1) / 2))[1]]
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = sorted(x for x in (num(s[1]) for s in use) if x is not None)
+        mx = [num(s[2]) for s in use if num(s[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in use for i in range(4) if s[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(use), "samples_in_timed_region": len(inside),
+                "power_w_max": max((num(s[3]) or 0.0) for s in use)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _shard(batch, ws, rank, shard):
+    if not shard:
+        return list(range(batch))
+    per = batch // ws
+    return list(range(rank * per, (rank + 1) * per))
+
+
+def _alg_bytes(x, om, backward):
+    """Algorithmic bytes of one call: forward x + om + y; backward
+    x + om + gy (reads) + gx + gom (writes).  y/gy/gx are x-sized, gom is om-sized."""
+    bx = x.numel() * x.element_size()
+    bo = om.numel() * om.element_size()
+    return (3 * bx + 2 * bo) if backward else (2 * bx + bo)
+
+
+def _traffic(workload, kind):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t[workload][kind]
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_inputs(cfg, images):
+    """The sample's inputs (same seeded generator as the GPU arm), as fp64 arrays."""
+    import oracle
+    import synth
+    oracle.build()
+    data = []
+    for (H, W, G) in cfg["stages"]:
+        g = oracle.Geometry(N=len(images), H=H, W=W, G=G, D=D)
+        x, om, gy = synth.make_case(len(images), H, W, G, D, H, W, K, 27 * G, cfg["dtype"],
+                                    images=images)
+        data.append((g, oracle._f64(x), oracle._f64(om), oracle._f64(gy)))
+    return data
+
+
+def oracle_sample(cfg, data):
+    """Time the fp64 oracle (as it stands) over `data`: every stage, forward (+ backward).
+    Returns seconds."""
+    import oracle
+    t0 = time.perf_counter()
+    for g, x, om, gy in data:
+        oracle.forward(g, x, om)
+        if cfg["backward"]:
+            oracle.backward(g, x, om, gy)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, target_s=12.0):
+    t1 = oracle_sample(cfg, oracle_inputs(cfg, [0, 1]))
+    n = int(max(2, min(cfg["batch"], round(2 * target_s / max(t1, 1e-3)))))
+    t = oracle_sample(cfg, oracle_inputs(cfg, list(range(n)))) if n > 2 else t1
+    return {"value": n / t, "unit": "imgs/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "kind": "oracle",
+            "sample": f"{n} images of workload {cfg['name']} (all stages, "
+                      f"{'fwd+bwd' if cfg['backward'] else 'fwd'}), fp64 C oracle, "
+                      f"OpenMP over (image, group), {t:.1f} s"}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    budget = 60.0
+    t2 = oracle_sample(cfg, oracle_inputs(cfg, [0, 1])) / 2
+    n = int(max(1, min(cfg["batch"], budget / max(1, args.steps + args.warmup) / max(t2, 1e-3))))
+    data = oracle_inputs(cfg, list(range(n)))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, data)
+    times = [oracle_sample(cfg, data) for _ in range(args.steps)]
+    tot = sum(times)
+    value = n * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "imgs/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong" if cfg["shard"] else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "desc": cfg["desc"], "global_batch": cfg["batch"],
+                   "images_per_step_sample": n},
+        "cpu_baseline": {"value": value, "unit": "imgs/s", "kind": "oracle",
+                         "cores": int(os.environ["OMP_NUM_THREADS"]),
+                         "sample": f"{n} images per step of workload {cfg['name']} "
+                                   f"(all stages, {'fwd+bwd' if cfg['backward'] else 'fwd'})"},
+        "e2e": {"value": value, "unit": "imgs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--global-batch", type=int, default=0)
+    ap.add_argument("--offsets", default="u2", choices=["u2", "zero", "u8", "smooth"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--out", default="", help="also append the JSON line to this file")
+    args = ap.parse_args()
+    cfg = dict(WORKLOADS[args.workload], name=args.workload)
+    if args.global_batch:
+        cfg["batch"] = args.global_batch
+    if args.warmup < 3:
+        args.warmup = 3  # contract: >= 3 untimed warm-up steps
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2401_06197_b200 as pkg
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    images = _shard(cfg["batch"], ws, rank, cfg["shard"])
+    n_img = len(images)
+    tdt = synth.DTYPES[cfg["dtype"]]
+
+    # ---- resident inputs / outputs (per-image seeds: any world size sees the same images)
+    stages = []
+    for (H, W, G) in cfg["stages"]:
+        x, om, gy = synth.make_case(n_img, H, W, G, D, H, W, K, 27 * G, cfg["dtype"],
+                                    images=images, offsets=args.offsets)
+        st = dict(H=H, W=W, G=G, x_cpu=x, om_cpu=om, gy_cpu=gy,
+                  x=x.to(dev), om=om.to(dev), gy=gy.to(dev))
+        st["y"] = torch.empty_like(st["x"])
+        if cfg["backward"]:
+            st["gx"] = torch.empty_like(st["x"])
+            st["gom"] = torch.empty_like(st["om"])
+            need = pkg.workspace_bytes(pkg.make_params(n_img, H, W, G, D), tdt)
+            st["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+        stages.append(st)
+
+    def calls(st):
+        out = [("fwd", lambda st=st: pkg.forward(st["x"], st["om"], group=st["G"], out=st["y"]))]
+        if cfg["backward"]:
+            out.append(("bwd", lambda st=st: pkg.backward(
+                st["x"], st["om"], st["gy"], group=st["G"], grad_input=st["gx"],
+                grad_offset_mask=st["gom"], workspace=st["ws"])))
+        return out
+
+    step_calls = [(si, kind, fn) for si, st in enumerate(stages) for kind, fn in calls(st)]
+
+    # ---- one eager step (outputs kept for verification outside the timed region)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        for _, _, fn in step_calls:
+            fn()
+    stream.synchronize()
+    verify = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.no_verify:
+        # cpu_baseline leg (the only place bench.py runs oracle/): first image vs fp64 oracle
+        verify = _verify(cfg, stages, images)
+    elif ws > 1 and not args.no_verify:
+        verify = _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist)
+
+    # ---- warm-up (eager), then capture K steps with event nodes between calls
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            for _, _, fn in step_calls:
+                fn()
+    stream.synchronize()
+    n_calls = len(step_calls)
+    evs = [torch.cuda.Event(enable_timing=True, external=True)
+           for _ in range(args.steps * n_calls + 1)]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        evs[0].record(stream)
+        e = 1
+        for _ in range(args.steps):
+            for _, _, fn in step_calls:
+                fn()
+                evs[e].record(stream)
+                e += 1
+    graph.replay()  # one untimed replay (graph upload, warm)
+    stream.synchronize()
+
+    uuid = None
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        pass
+    sampler = ClockSampler(uuid)
+    time.sleep(0.3)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.time()
+    with torch.cuda.stream(stream):
+        graph.replay()
+    torch.cuda.synchronize(dev)
+    t_wall1 = time.time()
+    if ws > 1:
+        dist.barrier()
+    time.sleep(0.1)
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+
+    total_ms = evs[0].elapsed_time(evs[-1])
+    durs = [evs[i].elapsed_time(evs[i + 1]) for i in range(len(evs) - 1)]
+    per_call = {}
+    for i, d in enumerate(durs):
+        si, kind, _ = step_calls[i % n_calls]
+        per_call.setdefault((si, kind), []).append(d)
+    ms_step_local = total_ms / args.steps
+    ms_step = ms_step_local
+    if ws > 1:
+        t = torch.tensor([ms_step_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = cfg["batch"] / (ms_step * 1e-3) if cfg["shard"] else ws * n_img / (ms_step * 1e-3)
+
+    # ---- per-stage table and roofline of the dominant kernel
+    peak, peak_src = _peaks()
+    table = []
+    kind_bytes, kind_ms = {}, {}
+    for si, st in enumerate(stages):
+        row = {"shape": f"{st['H']}x{st['W']}x{st['G'] * D} G{st['G']}", "images": n_img}
+        for kind in ("fwd", "bwd"):
+            if (si, kind) not in per_call:
+                continue
+            ms = sum(per_call[(si, kind)]) / len(per_call[(si, kind)])
+            b = _alg_bytes(st["x"], st["om"], kind == "bwd")
+            gbs = b / (ms * 1e-3) / 1e9
+            row[f"{kind}_us"] = round(ms * 1e3, 2)
+            row[f"{kind}_GBs"] = round(gbs, 1)
+            row[f"{kind}_frac"] = round(gbs / peak, 4)
+            kind_bytes[kind] = kind_bytes.get(kind, 0) + b
+            kind_ms[kind] = kind_ms.get(kind, 0.0) + ms
+        table.append(row)
+    dom = max(kind_ms, key=kind_ms.get)
+    launches_dom = len(stages)
+    achieved = kind_bytes[dom] / (kind_ms[dom] * 1e-3) / 1e9
+    share = kind_ms[dom] / sum(kind_ms.values())
+    roofline = {"bound": "hbm", "kernel": f"dcnv4 {dom} ({'zero-fill + ' if dom == 'bwd' else ''}"
+                                          f"{dom}_kernel), {launches_dom} launches per step",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                "traffic": _traffic(cfg["name"], dom), "share_of_step": round(share, 4),
+                "alg_bytes_per_launch": int(kind_bytes[dom] / launches_dom)}
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+
+    n_ours = (2 if cfg["backward"] else 1) * len(stages)
+    if cfg["backward"] and cfg["dtype"] != "f32":
+        n_ours += len(stages)  # fp32 -> half grad_input conversion
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "imgs/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong" if cfg["shard"] else "weak",
+        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": {"workload": cfg["name"], "desc": cfg["desc"], "global_batch": cfg["batch"],
+                   "per_gpu_batch": n_img, "stages": [f"{h}x{w}x{g * D} G{g}" for h, w, g in cfg["stages"]],
+                   "D": D, "kernel": "3x3 s1 p1 d1", "offset_scale": 1.0, "offsets": args.offsets,
+                   "parallelism": f"batch-sharded dp{ws}" if cfg["shard"] else f"replicas x{ws}",
+                   "l2": f"inputs larger than L2: per-rank working set "
+                         f"{sum(_alg_bytes(s['x'], s['om'], cfg['backward']) for s in stages) / 1e9:.2f} GB "
+                         f"per step vs 126 MB L2; no flush"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": n_ours * args.steps,
+        "gpu_launch_detail": f"per step: {len(stages)} fwd_kernel"
+                             + (f" + {len(stages)} bwd_kernel + {len(stages)} grad_input "
+                                f"zero-fill (cudaMemsetAsync)" if cfg["backward"] else "")
+                             + (f" + {len(stages)} convert_kernel" if cfg["backward"] and cfg["dtype"] != "f32" else ""),
+        "clocks": clocks,
+        "stages": table,
+        "parity": verify,
+        "wall_s_timed_region": round(t_wall1 - t_wall0, 4),
+    }
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(s + "\n")
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _verify(cfg, stages, images):
+    """Oracle check of the shard's first image on every stage (outside the timed region)."""
+    import numpy as np
+    import oracle
+    out = {}
+    tol = 1e-5 if cfg["dtype"] == "f32" else 1e-2
+    for st in stages:
+        g = oracle.Geometry(N=1, H=st["H"], W=st["W"], G=st["G"], D=D)
+        y_ref, y_abs = oracle.forward(g, st["x_cpu"][:1], st["om_cpu"][:1], with_abs=True)
+        errs = {"y": oracle.abs_scaled_error(st["y"][:1].cpu(), y_ref, y_abs)}
+        if cfg["backward"]:
+            gx_ref, gom_ref, gxa, goma = oracle.backward(g, st["x_cpu"][:1], st["om_cpu"][:1],
+                                                         st["gy_cpu"][:1], with_abs=True)
+            errs["grad_input"] = oracle.abs_scaled_error(st["gx"][:1].cpu(), gx_ref, gxa)
+            errs["grad_offset_mask"] = oracle.abs_scaled_error(st["gom"][:1].cpu(), gom_ref, goma)
+        out[f"{st['H']}x{st['W']}"] = {k: float(f"{v:.3e}") for k, v in errs.items()}
+    worst = max(v for e in out.values() for v in e.values())
+    return {"image": images[0], "max_abs_scaled_error": worst, "tol": tol,
+            "pass": bool(worst <= tol), "per_stage": out}
+
+
+def _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist):
+    """N > 1: gather (NCCL) every rank's first-image y and grad_offset_mask to rank 0, which
+    recomputes those images alone and requires bit-identical results (forward and
+    grad_offset_mask do not depend on the batch partition, R14)."""
+    import synth
+    ok = True
+    first = torch.tensor([images[0]], device=dev, dtype=torch.int64)
+    firsts = [torch.zeros_like(first) for _ in range(ws)]
+    dist.all_gather(firsts, first)
+    for st in stages:
+        for key in (("y", "gom") if cfg["backward"] else ("y",)):
+            mine = st[key][:1].contiguous()
+            got = [torch.empty_like(mine) for _ in range(ws)] if rank == 0 else None
+            dist.gather(mine, got, dst=0)
+            if rank != 0:
+                continue
+            for r in range(ws):
+                n = int(firsts[r].item())
+                x, om, gy = synth.make_case(1, st["H"], st["W"], st["G"], D, st["H"], st["W"], K,
+                                            27 * st["G"], cfg["dtype"], images=[n])
+                x, om, gy = x.to(dev), om.to(dev), gy.to(dev)
+                if key == "y":
+                    ref = pkg.forward(x, om, group=st["G"])
+                else:
+                    ref = pkg.backward(x, om, gy, group=st["G"])[1]
+                ok = ok and bool(torch.equal(ref, got[r]))
+    return {"cross_rank_bitexact": ok, "ranks": ws} if rank == 0 else None
+
+
+def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
+    """Same metric through the public API with pinned host buffers: every step copies the
+    step's inputs host->device and its results device->host inside the timed region."""
+    host = []
+    h2d = d2h = 0
+    for st in stages:
+        h = {"x": st["x_cpu"].pin_memory(), "om": st["om_cpu"].pin_memory(),
+             "gy": st["gy_cpu"].pin_memory(), "y": torch.empty_like(st["x_cpu"]).pin_memory()}
+        h2d += sum(h[k].numel() * h[k].element_size() for k in ("x", "om"))
+        d2h += h["y"].numel() * h["y"].element_size()
+        if cfg["backward"]:
+            h["gx"] = torch.empty_like(st["x_cpu"]).pin_memory()
+            h["gom"] = torch.empty_like(st["om_cpu"]).pin_memory()
+            h2d += h["gy"].numel() * h["gy"].element_size()
+            d2h += sum(h[k].numel() * h[k].element_size() for k in ("gx", "gom"))
+        host.append(h)
+
+    def step():
+        for st, h in zip(stages, host):
+            st["x"].copy_(h["x"], non_blocking=True)
+            st["om"].copy_(h["om"], non_blocking=True)
+            pkg.forward(st["x"], st["om"], group=st["G"], out=st["y"])
+            h["y"].copy_(st["y"], non_blocking=True)
+            if cfg["backward"]:
+                st["gy"].copy_(h["gy"], non_blocking=True)
+                pkg.backward(st["x"], st["om"], st["gy"], group=st["G"], grad_input=st["gx"],
+                             grad_offset_mask=st["gom"], workspace=st["ws"])
+                h["gx"].copy_(st["gx"], non_blocking=True)
+                h["gom"].copy_(st["gom"], non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        step()
+    stream.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            step()
+        b.record(stream)
+    stream.synchronize()
+    ms = a.elapsed_time(b) / args.e2e_steps
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_total = cfg["batch"] if cfg["shard"] else ws * len(stages[0]["x"])
+    return {"value": round(n_total / (ms * 1e-3), 2), "unit": "imgs/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(ms, 3), "steps": args.e2e_steps}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,10 @@
+"""B200-native (sm_100a) DCNv4 spatial aggregation (arxiv 2401.06197).
+
+The product is libdcnv4.so (C ABI, include/dcnv4.h); this package is its thin binding.
+"""
+from .binding import (DCNv4Error, DCNv4Function, Params, backward, dcnv4, forward,  # noqa: F401
+                    launch_info, lib, make_params, om_channels, output_size, workspace_bytes)
+
+__all__ = ["DCNv4Error", "DCNv4Function", "Params", "backward", "dcnv4", "forward",
+           "launch_info", "lib", "make_params", "om_channels", "output_size",
+           "workspace_bytes"]

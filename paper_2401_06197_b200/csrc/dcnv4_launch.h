@@ -1,0 +1,36 @@
+// dcnv4_launch.h -- internal host-side launch description shared by the API and the
+// per-dtype instantiation units (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace dcnv4 {
+
+struct Geo;
+
+struct Launch {
+  int nch;          // 16-B chunks per (pixel, group) = D*sizeof(T)/16
+  int cpl;          // chunks per lane
+  int lanes;        // nch / cpl lanes per (pixel, group)
+  int ppc;          // output pixels per CTA
+  int threads;      // CTA size (multiple of 32)
+  long long ctas;   // grid size
+  size_t smem;      // dynamic shared memory bytes
+  bool k33;         // compile-time 3x3 path
+  bool unit;        // offset_scale == 1 exact-split path
+  cudaStream_t stream;
+};
+
+#define DCNV4_DECLARE(SUFFIX)                                                              \
+  cudaError_t launch_fwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x,          \
+                                  const void* om, void* y);                                \
+  cudaError_t launch_bwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x,          \
+                                  const void* om, const void* gy, float* gx32, void* gom); \
+  cudaError_t launch_convert_##SUFFIX(const float* src, void* dst, long long nchunk,      \
+                                      cudaStream_t stream);
+
+DCNV4_DECLARE(f32)
+DCNV4_DECLARE(f16)
+DCNV4_DECLARE(bf16)
+
+}  // namespace dcnv4

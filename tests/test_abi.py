@@ -1,0 +1,129 @@
+"""The C-ABI library loads and exports every symbol include/dcnv4.h declares; host-only
+entry points (no CUDA call) behave as documented.  CPU only."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle
+import paper_2401_06197_b200 as pkg
+from paper_2401_06197_b200 import binding as b
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dcnv4.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    return re.findall(r"DCNV4_API\s+[\w\s\*]+?\b(dcnv4_\w+)\s*\(", src)
+
+
+def test_header_declares_the_boundary():
+    names = set(_declared())
+    assert {"dcnv4_forward", "dcnv4_backward", "dcnv4_output_size", "dcnv4_last_error",
+            "dcnv4_version", "dcnv4_backward_workspace_bytes", "dcnv4_launch_info"} <= names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(b.LIB_PATH)
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert pkg.lib().dcnv4_version() == 100
+
+
+def test_params_struct_layout():
+    assert ctypes.sizeof(b.Params) == 80
+    assert b.Params.offset_scale.offset == 64 and b.Params.softmax.offset == 72
+
+
+@pytest.mark.parametrize("k,s,p,d", [((3, 3), (1, 1), (1, 1), (1, 1)), ((3, 3), (2, 2), (1, 1), (1, 1)),
+                                     ((5, 3), (1, 2), (2, 0), (1, 2)), ((1, 1), (1, 1), (0, 0), (1, 1)),
+                                     ((2, 2), (1, 1), (0, 1), (1, 1)), ((3, 3), (2, 1), (0, 2), (2, 2))])
+def test_output_size_matches_conv_arithmetic(k, s, p, d):
+    for H, W in [(7, 9), (56, 56), (200, 320), (1, 5)]:
+        g = oracle.Geometry(N=2, H=H, W=W, G=2, D=16, kh=k[0], kw=k[1], sh=s[0], sw=s[1],
+                            ph=p[0], pw=p[1], dh=d[0], dw=d[1])
+        Ho, Wo = g.out_hw()
+        prm = b.make_params(2, H, W, 2, 16, k, s, p, d)
+        if Ho <= 0 or Wo <= 0:
+            with pytest.raises(b.DCNv4Error):
+                b.output_size(prm)
+            continue
+        assert b.output_size(prm) == (Ho, Wo)
+
+
+def _status(fn, *args):
+    return fn(*args)
+
+
+def test_validation_errors_name_the_axis():
+    L = pkg.lib()
+    P = b.make_params
+    cases = [
+        (P(1, 8, 8, 2, 6), 0, b.ERR_UNSUPPORTED, "group channel"),    # 24 B not a multiple of 16
+        (P(1, 8, 8, 2, 8), 1, b.OK, ""),                                 # f16 D=8 -> 16 B ok
+        (P(1, 8, 8, 0, 16), 0, b.ERR_INVALID_ARG, "G"),
+        (P(1, 0, 8, 2, 16), 0, b.ERR_INVALID_ARG, "H"),
+        (P(1, 8, 8, 2, 16, om_stride=10), 0, b.ERR_SHAPE, "om_stride"),
+        (P(1, 2, 2, 2, 16, kernel_size=5, pad=0), 0, b.ERR_SHAPE, "H axis"),
+        (P(1, 8, 8, 2, 16, kernel_size=9), 0, b.ERR_UNSUPPORTED, "K"),
+        (P(1, 8, 8, 2, 128), 0, b.ERR_UNSUPPORTED, "exceeds 256"),
+        (P(1, 8, 8, 2, 16, offset_scale=float("nan")), 0, b.ERR_INVALID_ARG, "offset_scale"),
+    ]
+    for prm, dt, code, word in cases:
+        rc = L.dcnv4_launch_info(ctypes.byref(prm), dt, 0, None, None, None, None, None)
+        assert rc == code, (prm.D, prm.G, code, rc, L.dcnv4_last_error())
+        if code:
+            assert word in L.dcnv4_last_error().decode()
+    assert L.dcnv4_forward(None, 0, None, None, None, None) == b.ERR_INVALID_ARG
+    assert L.dcnv4_forward(ctypes.byref(P(1, 8, 8, 2, 16)), 7, None, None, None, None) == b.ERR_INVALID_ARG
+    # NULL / misaligned pointers are rejected before any CUDA call
+    prm = P(1, 8, 8, 2, 16)
+    assert L.dcnv4_forward(ctypes.byref(prm), 0, None, ctypes.c_void_p(16), ctypes.c_void_p(16), None) == b.ERR_INVALID_ARG
+    assert L.dcnv4_forward(ctypes.byref(prm), 0, ctypes.c_void_p(8), ctypes.c_void_p(16),
+                           ctypes.c_void_p(16), None) == b.ERR_MISALIGNED
+    # N = 0 is a no-op (no launch)
+    assert L.dcnv4_forward(ctypes.byref(P(0, 8, 8, 2, 16)), 0, None, None, None, None) == b.OK
+    assert L.dcnv4_backward(ctypes.byref(P(0, 8, 8, 2, 16)), 0, None, None, None, None, None,
+                            None, 0, None) == b.OK
+
+
+def test_workspace_contract():
+    prm = b.make_params(2, 8, 8, 2, 16)
+    import torch
+    assert b.workspace_bytes(prm, torch.float32) == 0
+    assert b.workspace_bytes(prm, torch.float16) == 2 * 8 * 8 * 32 * 4
+    L = pkg.lib()
+    rc = L.dcnv4_backward(ctypes.byref(b.make_params(1, 8, 8, 2, 16)), 1, ctypes.c_void_p(16),
+                          ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(16),
+                          ctypes.c_void_p(16), None, 0, None)
+    assert rc == b.ERR_WORKSPACE
+
+
+def test_launch_shape():
+    import torch
+    # InternImage-T stage 1 (c2): C=64, G=4, D=16
+    prm = b.make_params(64, 56, 56, 4, 16)
+    fi = b.launch_info(prm, torch.float32)
+    assert fi["lanes"] * fi["chunks_per_lane"] == 4   # 64 B per (pixel, group) = 4 chunks
+    assert fi["threads_per_cta"] % 32 == 0 and fi["threads_per_cta"] <= 256
+    assert fi["ctas"] * fi["pixels_per_cta"] >= 64 * 56 * 56
+    hi = b.launch_info(prm, torch.float16)
+    assert hi["lanes"] * hi["chunks_per_lane"] == 2
+    # G = 80 (c5 stage 3) stays within one CTA per pixel
+    big = b.launch_info(b.make_params(32, 16, 16, 80, 16), torch.bfloat16, backward=True)
+    assert big["threads_per_cta"] <= 256
+
+
+def test_product_path_has_no_oracle_or_cpu_fallback():
+    """The product package never imports the oracle, and refuses CPU tensors."""
+    import torch
+    pkg_dir = os.path.join(ROOT, "paper_2401_06197_b200")
+    for dirpath, _, files in os.walk(pkg_dir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in src.replace("no oracle", ""), f
+    with pytest.raises(ValueError):
+        pkg.forward(torch.zeros(1, 4, 4, 32), torch.zeros(1, 4, 4, 54), group=2)

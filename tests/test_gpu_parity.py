@@ -1,0 +1,291 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by
+element, with the abs-scaled error metric of SURVEY.md 8(c).4:
+
+    e_i = |gpu_i - ref_i| / (A_i + 1e-30 max A),  A = oracle magnitude pass,
+    fp32: max e <= 1e-5 (north star);  fp16 / bf16: max e <= 1e-2.
+
+The oracle is fed exactly the values the GPU sees (storage dtype -> fp64).  Offset
+gradients whose fp64 sampling coordinate lies within 1e-5 of an integer (a kink, where
+several sub-gradients are valid) are masked; the number masked is reported.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2401_06197_b200 as pkg
+from tests.helpers import pack_om, unpack_om
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-5, "f16": 1e-2, "bf16": 1e-2}
+TDT = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+
+
+def _geom(N, H, W, G, D, k=(3, 3), s=(1, 1), p=(1, 1), d=(1, 1), scale=1.0, S=0, softmax=False):
+    return oracle.Geometry(N=N, H=H, W=W, G=G, D=D, kh=k[0], kw=k[1], sh=s[0], sw=s[1], ph=p[0],
+                           pw=p[1], dh=d[0], dw=d[1], offset_scale=scale, om_stride=S,
+                           softmax=softmax)
+
+
+def _kink_mask(g: oracle.Geometry, om64: np.ndarray, eps=1e-5):
+    """True for offset channels whose fp64 coordinate is within eps of an integer."""
+    Ho, Wo = g.out_hw()
+    K = g.K
+    cy, cx = g.dh * (g.kh - 1) // 2, g.dw * (g.kw - 1) // 2
+    dx, dy, _ = unpack_om(om64, g.G, K)
+    k = np.arange(K)
+    i, j = k // g.kh, k % g.kh
+    ho = np.arange(Ho).reshape(1, Ho, 1, 1, 1)
+    wo = np.arange(Wo).reshape(1, 1, Wo, 1, 1)
+    py = (ho * g.sh - g.ph + cy) + g.offset_scale * ((j * g.dh - cy) + dy)
+    px = (wo * g.sw - g.pw + cx) + g.offset_scale * ((i * g.dw - cx) + dx)
+    fy = np.abs(py - np.round(py)) < eps
+    fx = np.abs(px - np.round(px)) < eps
+    mask = np.zeros(om64.shape, bool)
+    body = np.zeros(om64.shape[:3] + (g.G, 3 * K), bool)
+    body[..., 0:2 * K:2] = fx
+    body[..., 1:2 * K:2] = fy
+    mask[..., :3 * g.G * K] = body.reshape(om64.shape[:3] + (3 * g.G * K,))
+    return mask
+
+
+def _err(gpu, ref, scale, mask=None):
+    gpu = gpu.detach().double().cpu().numpy() if torch.is_tensor(gpu) else gpu
+    den = scale + 1e-30 * max(scale.max(initial=0.0), 1e-300)
+    e = np.abs(gpu - ref) / den
+    if mask is not None:
+        e = np.where(mask, 0.0, e)
+    return float(e.max(initial=0.0))
+
+
+def run_case(g: oracle.Geometry, dtype="f32", offsets="u2", images=None, backward=True,
+             inputs=None, check_images=None):
+    """Run fwd (+bwd) on the GPU for the whole batch; compare `check_images` (default all)
+    against the oracle.  Returns the dict of max errors."""
+    dev = torch.device("cuda:0")
+    Ho, Wo = g.out_hw()
+    if inputs is None:
+        x, om, gy = synth.make_case(g.N, g.H, g.W, g.G, g.D, Ho, Wo, g.K, g.S, dtype,
+                                    images=images, offsets=offsets)
+    else:
+        x, om, gy = inputs
+    xd, omd, gyd = x.to(dev), om.to(dev), gy.to(dev)
+    kw = dict(group=g.G, kernel_size=(g.kh, g.kw), stride=(g.sh, g.sw), pad=(g.ph, g.pw),
+              dilation=(g.dh, g.dw), offset_scale=g.offset_scale, softmax=g.softmax)
+    y = pkg.forward(xd, omd, **kw)
+    if backward:
+        gx, gom = pkg.backward(xd, omd, gyd, **kw)
+    torch.cuda.synchronize()
+    sel = list(range(g.N)) if check_images is None else list(check_images)
+    gs = oracle.Geometry(**{**g.__dict__, "N": len(sel)})
+    xs, oms, gys = x[sel], om[sel], gy[sel]
+    y_ref, y_abs = oracle.forward(gs, xs, oms, with_abs=True)
+    out = {"y": _err(y[sel], y_ref, y_abs)}
+    if backward:
+        gx_ref, gom_ref, gx_abs, gom_abs = oracle.backward(gs, xs, oms, gys, with_abs=True)
+        mask = _kink_mask(gs, oms.double().numpy())
+        out["grad_input"] = _err(gx[sel], gx_ref, gx_abs)
+        out["grad_offset_mask"] = _err(gom[sel], gom_ref, gom_abs, mask)
+        out["masked"] = int(mask.sum())
+        pad = gom[sel][..., 3 * g.G * g.K:]
+        assert not pad.any(), "padding channels of grad_offset_mask must be written 0"
+    return out
+
+
+def _assert_tol(errs, dtype):
+    tol = TOL[dtype]
+    bad = {k: v for k, v in errs.items() if k != "masked" and not (v <= tol)}
+    assert not bad, f"{dtype}: {errs}"
+
+
+# ---------------------------------------------------------------- small configs
+CASES = [
+    # (id, geometry, offsets)
+    ("c1_tiny", _geom(1, 8, 8, 2, 16), "u2"),
+    ("ragged", _geom(3, 13, 17, 3, 16), "u2"),
+    ("stride2_pad0", _geom(2, 15, 14, 2, 16, s=(2, 2), p=(0, 0)), "u2"),
+    ("dil2_pad2", _geom(2, 12, 11, 4, 16, p=(2, 2), d=(2, 2)), "u2"),
+    ("k5x5", _geom(1, 10, 9, 2, 16, k=(5, 5), p=(2, 2)), "u2"),
+    ("k3x5_s1x2", _geom(2, 9, 12, 2, 16, k=(3, 5), s=(1, 2), p=(1, 2)), "u2"),
+    ("k1x1", _geom(2, 7, 7, 2, 16, k=(1, 1), p=(0, 0)), "u2"),
+    ("k2x2_even", _geom(1, 9, 8, 2, 16, k=(2, 2), p=(0, 1)), "u2"),
+    ("scale0.5", _geom(2, 11, 10, 2, 16, scale=0.5), "u2"),
+    ("scale2", _geom(2, 11, 10, 2, 16, scale=2.0), "u2"),
+    ("om_stride_pad", _geom(2, 9, 10, 3, 16, S=3 * 3 * 9 + 5), "u2"),
+    ("om_stride_pad8", _geom(2, 9, 10, 2, 16, S=56), "u2"),
+    ("zero_offsets_kinks", _geom(2, 10, 10, 2, 16), "zero"),
+    ("u8_offsets", _geom(2, 12, 12, 2, 16), "u8"),
+    ("smooth_offsets", _geom(2, 16, 16, 4, 16), "smooth"),
+    ("D32", _geom(2, 10, 9, 2, 32), "u2"),
+    ("D64", _geom(1, 8, 9, 2, 64), "u2"),
+    ("G1", _geom(2, 9, 9, 1, 16), "u2"),
+    ("G80_wide", _geom(1, 5, 6, 80, 16), "u2"),
+    ("softmax_v3", _geom(2, 9, 10, 2, 16, softmax=True), "u2"),
+    ("softmax_k5", _geom(1, 8, 9, 2, 16, k=(5, 5), p=(2, 2), softmax=True), "u2"),
+    ("single_pixel", _geom(1, 1, 1, 2, 16), "u2"),
+]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16", "bf16"])
+@pytest.mark.parametrize("name,g,offsets", CASES, ids=[c[0] for c in CASES])
+def test_parity_small(name, g, offsets, dtype):
+    _assert_tol(run_case(g, dtype, offsets), dtype)
+
+
+@pytest.mark.parametrize("dtype,D", [("f32", 4), ("f32", 8), ("f16", 8), ("bf16", 8), ("f16", 128),
+                                     ("bf16", 24)])
+def test_parity_channel_widths(dtype, D):
+    g = _geom(2, 9, 7, 3, D)
+    _assert_tol(run_case(g, dtype), dtype)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+def test_all_out_of_bounds_and_huge_offsets(dtype):
+    """dp = +3H everywhere: y = 0, grad = 0.  Then NaN / 1e30 offsets on some pixels:
+    no crash, and every other pixel still matches (reading R12)."""
+    g = _geom(1, 6, 7, 2, 16)
+    Ho, Wo = g.out_hw()
+    x, om, gy = synth.make_case(1, 6, 7, 2, 16, Ho, Wo, 9, g.S, dtype)
+    dx, dy, m = unpack_om(om.double().numpy(), 2, 9)
+    far = torch.from_numpy(pack_om(dx + 18.0, dy - 18.0, m)).to(TDT[dtype])
+    errs = run_case(g, dtype, inputs=(x, far, gy))
+    _assert_tol(errs, dtype)
+    dev = torch.device("cuda:0")
+    y = pkg.forward(x.to(dev), far.to(dev), group=2)
+    assert not y.any()
+    bad = om.clone()
+    bad[0, 0, 0, 0] = float("nan")
+    bad[0, 1, 1, 1] = 1e30 if dtype == "f32" else float("inf")
+    yb = pkg.forward(x.to(dev), bad.to(dev), group=2)
+    gxb, gomb = pkg.backward(x.to(dev), bad.to(dev), gy.to(dev), group=2)
+    torch.cuda.synchronize()
+    yr = pkg.forward(x.to(dev), om.to(dev), group=2)
+    # pixels other than the two poisoned (pixel, group) rows are unaffected
+    keep = torch.ones(Ho, Wo, 2, dtype=torch.bool)
+    keep[0, 0, 0] = False
+    keep[1, 1, 0] = False
+    keep = keep.repeat_interleave(16, -1).to(dev)
+    assert torch.equal(yb[0][keep], yr[0][keep])
+
+
+def test_empty_batch_is_noop():
+    dev = torch.device("cuda:0")
+    x = torch.zeros(0, 8, 8, 32, device=dev)
+    om = torch.zeros(0, 8, 8, 54, device=dev)
+    y = pkg.forward(x, om, group=2)
+    gx, gom = pkg.backward(x, om, torch.zeros(0, 8, 8, 32, device=dev), group=2)
+    assert y.shape == (0, 8, 8, 32) and gx.shape == x.shape and gom.shape == om.shape
+
+
+def test_forward_and_grad_om_bit_deterministic():
+    g = _geom(4, 28, 28, 8, 16)
+    Ho, Wo = g.out_hw()
+    dev = torch.device("cuda:0")
+    x, om, gy = (t.to(dev) for t in synth.make_case(4, 28, 28, 8, 16, Ho, Wo, 9, g.S, "f32"))
+    y1 = pkg.forward(x, om, group=8)
+    y2 = pkg.forward(x, om, group=8)
+    _, g1 = pkg.backward(x, om, gy, group=8)
+    _, g2 = pkg.backward(x, om, gy, group=8)
+    assert torch.equal(y1, y2) and torch.equal(g1, g2)
+
+
+def test_autograd_function_matches_direct_calls():
+    g = _geom(2, 9, 9, 2, 16)
+    Ho, Wo = g.out_hw()
+    dev = torch.device("cuda:0")
+    x, om, gy = (t.to(dev) for t in synth.make_case(2, 9, 9, 2, 16, Ho, Wo, 9, g.S, "f32"))
+    xr = x.clone().requires_grad_(True)
+    omr = om.clone().requires_grad_(True)
+    y = pkg.dcnv4(xr, omr, 2)
+    y.backward(gy)
+    gx, gom = pkg.backward(x, om, gy, group=2)
+    assert torch.equal(y.detach(), pkg.forward(x, om, group=2))
+    assert torch.equal(omr.grad, gom)
+    torch.testing.assert_close(xr.grad, gx, rtol=1e-6, atol=1e-6)
+
+
+def test_cuda_graph_capture_replays():
+    """The C-ABI calls are stream-async and capturable (bench.py times graph replays)."""
+    g = _geom(2, 14, 14, 4, 16)
+    Ho, Wo = g.out_hw()
+    dev = torch.device("cuda:0")
+    x, om, gy = (t.to(dev) for t in synth.make_case(2, 14, 14, 4, 16, Ho, Wo, 9, g.S, "f16"))
+    y = torch.empty_like(x)
+    gx = torch.empty_like(x)
+    gom = torch.empty_like(om)
+    ws = torch.empty(pkg.workspace_bytes(pkg.make_params(2, 14, 14, 4, 16), torch.float16),
+                     dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        pkg.forward(x, om, group=4, out=y)
+        pkg.backward(x, om, gy, group=4, grad_input=gx, grad_offset_mask=gom, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        pkg.forward(x, om, group=4, out=y)
+        pkg.backward(x, om, gy, group=4, grad_input=gx, grad_offset_mask=gom, workspace=ws)
+    y.zero_(); gx.zero_(); gom.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, pkg.forward(x, om, group=4))
+    _, gom2 = pkg.backward(x, om, gy, group=4)
+    assert torch.equal(gom, gom2)
+
+
+# ---------------------------------------------------------------- full-size configs
+# BASELINE.json configs at full size, in the launch configuration bench.py times; the
+# oracle checks the first and last image, invariants check the whole batch.
+STAGES_224 = [(56, 56, 4), (28, 28, 8), (14, 14, 16), (7, 7, 32)]       # c2 / c4, D=16
+STAGES_800 = [(200, 320, 4), (100, 160, 8), (50, 80, 16), (25, 40, 32)]  # c3, D=16
+STAGES_UNET = [(64, 64, 20), (32, 32, 40), (16, 16, 80)]                # c5, D=16
+
+
+def _full(N, H, W, G, dtype, backward, sample):
+    g = _geom(N, H, W, G, 16)
+    errs = run_case(g, dtype, backward=backward, check_images=sample)
+    _assert_tol(errs, dtype)
+    return errs
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+@pytest.mark.parametrize("H,W,G", STAGES_224)
+def test_c2_full_forward(H, W, G, dtype):
+    _full(64, H, W, G, dtype, False, [0, 63])
+
+
+@pytest.mark.parametrize("H,W,G", STAGES_800)
+def test_c3_full_forward_f16(H, W, G):
+    _full(8, H, W, G, "f16", False, [0, 7])
+
+
+@pytest.mark.parametrize("H,W,G", STAGES_224)
+def test_c4_full_fwd_bwd_f32(H, W, G):
+    _full(512, H, W, G, "f32", True, [0, 511])
+
+
+@pytest.mark.parametrize("H,W,G", STAGES_UNET)
+def test_c5_full_fwd_bwd_bf16(H, W, G):
+    _full(32, H, W, G, "bf16", True, [0, 31])
+
+
+@pytest.mark.parametrize("H,W,G", STAGES_224[:2])
+def test_full_batch_invariants(H, W, G):
+    """Whole-batch checks the oracle cannot afford: adjoint <gy, y> = <gx, x> and Euler
+    sum m * grad_m = <gy, y>, evaluated in fp64 from the device results (c.3 #4)."""
+    N = 512
+    Ho, Wo = H, W
+    dev = torch.device("cuda:0")
+    x, om, gy = (t.to(dev) for t in synth.make_case(N, H, W, G, 16, Ho, Wo, 9, 27 * G, "f32"))
+    y = pkg.forward(x, om, group=G)
+    gx, gom = pkg.backward(x, om, gy, group=G)
+    lhs = (gy.double() * y.double()).sum().item()
+    rhs = (gx.double() * x.double()).sum().item()
+    m = om.view(N, Ho, Wo, G, 27)[..., 18:].double()
+    gm = gom.view(N, Ho, Wo, G, 27)[..., 18:].double()
+    euler = (m * gm).sum().item()
+    scale = (gy.double().abs() * y.double().abs()).sum().item()
+    assert abs(lhs - rhs) <= 1e-5 * scale
+    assert abs(lhs - euler) <= 1e-5 * scale
