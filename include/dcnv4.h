@@ -62,8 +62,8 @@ typedef enum {
   DCNV4_OK = 0,
   DCNV4_ERR_INVALID_ARG = 1, /* NULL pointer, non-positive size, bad enum, bad flag     */
   DCNV4_ERR_SHAPE = 2,       /* empty output, om_stride < 3GK, per-image size >= 2^31   */
-  DCNV4_ERR_UNSUPPORTED = 3, /* D*sizeof(T) not a multiple of 16 or > 256 B, K > 64,
-                                G*lanes > 1024                                          */
+  DCNV4_ERR_UNSUPPORTED = 3, /* D*sizeof(T) not 16 B x a power of two or > 256 B, K > 64,
+                                G*lanes > 256                                           */
   DCNV4_ERR_MISALIGNED = 4,  /* x / y / grad pointers not 16-B aligned, om not T-aligned */
   DCNV4_ERR_WORKSPACE = 5,   /* backward workspace missing or too small                 */
   DCNV4_ERR_CUDA = 6         /* a launch failed; the CUDA error string is in last_error */

@@ -156,7 +156,7 @@ def abs_scaled_error(gpu, ref, scale) -> float:
     gpu = _f64(gpu)
     ref = _f64(ref)
     scale = _f64(scale)
-    den = scale + 1e-30 * max(float(scale.max(initial=0.0)), 1e-300)
+    den = scale + max(1e-30 * float(scale.max(initial=0.0)), 1e-300)
     if gpu.size == 0:
         return 0.0
     return float((np.abs(gpu - ref) / den).max())

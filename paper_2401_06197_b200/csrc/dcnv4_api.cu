@@ -97,6 +97,11 @@ int validate_geometry(const dcnv4_params* p, int dtype, int64_t* Ho, int64_t* Wo
   if ((int64_t)p->D * b > 256)
     return fail(DCNV4_ERR_UNSUPPORTED, "D*sizeof(dtype) = %lld bytes exceeds 256",
                 (long long)p->D * b);
+  const int64_t nch = (int64_t)p->D * b / 16;
+  if (nch & (nch - 1))
+    return fail(DCNV4_ERR_UNSUPPORTED,
+                "D*sizeof(dtype) = %lld bytes is not 16 B times a power of two (group channel axis)",
+                (long long)p->D * b);
   return DCNV4_OK;
 }
 
