@@ -63,7 +63,7 @@ typedef enum {
   DCNV4_ERR_INVALID_ARG = 1, /* NULL pointer, non-positive size, bad enum, bad flag     */
   DCNV4_ERR_SHAPE = 2,       /* empty output, om_stride < 3GK, per-image size >= 2^31   */
   DCNV4_ERR_UNSUPPORTED = 3, /* D*sizeof(T) not 16 B x a power of two or > 256 B, K > 64,
-                                G*lanes > 256                                           */
+                                offset_mask tile larger than shared memory              */
   DCNV4_ERR_MISALIGNED = 4,  /* x / y / grad pointers not 16-B aligned, om not T-aligned */
   DCNV4_ERR_WORKSPACE = 5,   /* backward workspace missing or too small                 */
   DCNV4_ERR_CUDA = 6         /* a launch failed; the CUDA error string is in last_error */
@@ -118,8 +118,8 @@ DCNV4_API int dcnv4_backward(const dcnv4_params *p, dcnv4_dtype dtype, const voi
                    void *grad_offset_mask, void *workspace, size_t workspace_bytes,
                    void *stream);
 
-/* Launch-shape introspection used by the harness (lanes per (pixel, group), channels
- * per lane, pixels per CTA, threads per CTA, CTAs) for forward (pass = 0) or backward
+/* Launch-shape introspection used by the harness (lanes per (pixel, group), 16-B chunks
+ * per lane, output pixels per CTA tile, threads per CTA, CTAs) for forward (pass = 0) or backward
  * (pass = 1).  Host-only.                                                             */
 DCNV4_API int dcnv4_launch_info(const dcnv4_params *p, dcnv4_dtype dtype, int pass, int32_t *lanes,
                       int32_t *chunks_per_lane, int32_t *pixels_per_cta,

@@ -6,6 +6,10 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
+#include <cudaTypedefs.h>
+
 #include "../../include/dcnv4.h"
 #include "dcnv4_kernels.cuh"
 #include "dcnv4_launch.h"
@@ -26,7 +30,6 @@ int elem_size(int dtype) { return dtype == DCNV4_F32 ? 4 : 2; }
 
 constexpr int kMaxK = 64;           // largest kernel_h*kernel_w supported
 constexpr int kMaxThreads = 256;    // CTA size bound (__launch_bounds__)
-constexpr int kTargetThreads = 256;
 
 // Default chunks-per-lane for a given chunk count; the harness may override it with the
 // env vars DCNV4_FWD_CPL / DCNV4_BWD_CPL (ablation only).
@@ -105,8 +108,225 @@ int validate_geometry(const dcnv4_params* p, int dtype, int64_t* Ho, int64_t* Wo
   return DCNV4_OK;
 }
 
-int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t Wo,
+// Average 128-bit load wavefronts per 8-lane phase relative to the ideal (1.0 = every
+// phase hits 8 distinct bank quads) for a CTA whose threads are ordered
+// (pixel, group, lane) with Gc groups and L lanes per (pixel, group); tries the chunk
+// stagger shifts and returns the best (rot = (pg_in_warp >> shift) & (CPL-1)).
+double conflict_factor(int Gc, int L, int cpl, int nch, int threads, int* best_shift) {
+  double best = 1e30;
+  *best_shift = -1;
+  for (int rs = -1; rs <= 4; ++rs) {
+    double wf = 0, ideal = 0;
+    for (int t0 = 0; t0 < threads; t0 += 8) {
+      for (int c = 0; c < cpl; ++c) {
+        int count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int active = 0, mx = 0;
+        for (int l = 0; l < 8 && t0 + l < threads; ++l) {
+          const int t = t0 + l;
+          const int lg = t % L, q = t / L, gl = q % Gc;
+          const int pg = (t & 31) / L;
+          const int rot = rs < 0 ? 0 : (pg >> rs) & (cpl - 1);
+          const int ch = ((c + rot) & (cpl - 1)) * L + lg;
+          const int quad = (gl * nch + ch) & 7;
+          mx = ++count[quad] > mx ? count[quad] : mx;
+          ++active;
+        }
+        if (active) { wf += mx; ideal += (active + 7) / 8; }
+      }
+    }
+    const double f = wf / ideal;
+    if (f < best - 1e-9) { best = f; *best_shift = rs; }
+  }
+  return best;
+}
+
+struct TileChoice {
+  int TH, TW, Gc, rot_shift;
+};
+
+// CTA tile: minimise (L2->L1 footprint traffic) + (bank-conflict excess) + (idle lanes)
+// + (per-CTA overhead), all in bytes-equivalent.  DESIGN.md "Tiling".
+dcnv4::FastDiv make_fastdiv(unsigned d) {
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;
+  const unsigned long long mf = ((1ull << (32 + l)) + d - 1) / d;
+  return {(unsigned)(mf - (1ull << 32)), l};
+}
+
+// Halo box (TMA path): rows/cols of input the tile's samples need with |offset| < 2 px.
+inline int halo_rows(const dcnv4_params* p, int TH) {
+  return (TH - 1) * p->stride_h + (p->kernel_h - 1) * p->dilation_h + 5;
+}
+inline int halo_cols(const dcnv4_params* p, int TW) {
+  return (TW - 1) * p->stride_w + (p->kernel_w - 1) * p->dilation_w + 5;
+}
+constexpr size_t kHaloSmemBudget = 110 * 1024;  // two CTAs per SM
+
+size_t seg_bytes_for(int Gc, int K, int b) {
+  int sb = ((Gc * 3 * K * b) + 15) & ~15;
+  if ((sb / 16) % 2 == 0) sb += 16;
+  return (size_t)sb;
+}
+
+size_t halo_smem(const dcnv4_params* p, int TH, int TW, int Gc, int b) {
+  const size_t PB = (size_t)Gc * p->D * b;
+  const size_t hb = ((size_t)halo_rows(p, TH) * halo_cols(p, TW) * PB + 127) & ~(size_t)127;
+  return 2 * hb + 2 * (size_t)TH * TW * seg_bytes_for(Gc, p->kernel_h * p->kernel_w, b) + 16;
+}
+
+TileChoice choose_tile(const dcnv4_params* p, int b, int nch, int cpl, int64_t Ho, int64_t Wo,
+                       bool halo) {
+  const int L = nch / cpl;
+  const int G = p->G;
+  const double V = nch * 16.0;  // bytes of one (pixel, group) channel vector
+  const double K = (double)p->kernel_h * p->kernel_w;
+  const double kappa = 3.0;     // L2->L1 byte vs L1-hit byte
+  TileChoice best = {1, 1, G, -1};
+  double best_cost = 1e300;
+  const char* env = getenv("DCNV4_TILE");
+  int fth = 0, ftw = 0, fgc = 0;
+  if (env && *env) sscanf(env, "%d,%d,%d", &fth, &ftw, &fgc);
+  const int cand[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 20, 24, 25, 28, 32, 40, 50, 56, 64};
+  const double total_pg = (double)p->N * Ho * Wo * G;
+  for (int Gc = 1; Gc <= G; ++Gc) {
+    if (G % Gc || Gc * L > kMaxThreads) continue;
+    if (fgc && Gc != fgc) continue;
+    int shift;
+    const double cf = conflict_factor(Gc, L, cpl, nch, 128 > Gc * L ? 128 : Gc * L, &shift);
+    for (int TH : cand) {
+      if (TH > Ho || (fth && TH != fth)) continue;
+      for (int TW : cand) {
+        if (TW > Wo || (ftw && TW != ftw)) continue;
+        const int thr = TH * TW * Gc * L;
+        if (thr > kMaxThreads) break;
+        const bool whole = TH == Ho && TW == Wo;
+        if (thr < 64 && !whole && !(fth && ftw)) continue;
+        const double tiles = (double)((Ho + TH - 1) / TH) * ((Wo + TW - 1) / TW) * (G / Gc) * p->N;
+        double fh = halo_rows(p, TH), fw = halo_cols(p, TW);
+        double cfe = cf;
+        if (halo) {  // the whole box is fetched (zero-filled outside the image)
+          if (fh > 256 || fw > 256 || halo_smem(p, TH, TW, Gc, b) > kHaloSmemBudget) continue;
+          if (((size_t)Gc * p->D * b) % 128) cfe += 0.5;  // pixel pitch breaks the quad pattern
+        } else {
+          fh = std::min<double>(fh, p->H);
+          fw = std::min<double>(fw, p->W);
+        }
+        const double idle = tiles * TH * TW * Gc - total_pg;
+        const double l1 = total_pg * 4.0 * K * V;
+        const double cost = tiles * kappa * fh * fw * Gc * V + (cfe - 1.0) * l1 +
+                            idle * 4.0 * K * V * 0.25 + tiles * 4096.0 +
+                            (thr % 32 ? (32 - thr % 32) : 0) * tiles * 64.0;
+        if (cost < best_cost) {
+          best_cost = cost;
+          best = {TH, TW, Gc, shift};
+        }
+      }
+    }
+  }
+  (void)b;
+  return best;
+}
+
+// TMA descriptor of x as a 4-D tensor {C, W, H, N} (innermost first) with a
+// {Gc*D, HW, HH, 1} box; out-of-image elements are zero-filled by the hardware.
+bool encode_x_map(const dcnv4_params* p, int dtype, const void* x, int box_c, int box_w,
+                  int box_h, CUtensorMap* map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const int b = elem_size(dtype);
+  const cuuint64_t C = (cuuint64_t)p->G * p->D;
+  const cuuint64_t dims[4] = {C, (cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->N};
+  const cuuint64_t strides[3] = {C * b, C * b * p->W, C * b * p->W * p->H};
+  const cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUtensorMapDataType dt = dtype == DCNV4_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : dtype == DCNV4_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                      : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUresult r = encode(map, dt, 4, const_cast<void*>(x), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Forward on the paper's grid (3x3, stride 1, dilation 1): the TMA halo kernel with
+// compile-time strides (dcnv4_kernels.cuh fwd33_kernel).  Fills lc/g and returns true
+// when the geometry, alignment and shared-memory budget allow it; the caller otherwise
+// keeps the global-gather kernel.  `x` may be NULL (planning only, lc->halo stays false).
+bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const void* x,
                 dcnv4::Launch* lc, dcnv4::Geo* g) {
+  const char* path = getenv("DCNV4_FWD_PATH");
+  if (path && path[0] == 'g') return false;
+  if (p->kernel_h != 3 || p->kernel_w != 3 || p->stride_h != 1 || p->stride_w != 1 ||
+      p->dilation_h != 1 || p->dilation_w != 1)
+    return false;
+  const int b = elem_size(dtype);
+  const int nch = lc->nch, cpl = lc->cpl, L = lc->lanes;
+  const int GC = nch >= 8 ? 1 : 8 / nch;
+  if (p->G % GC) return false;
+  const int PB = GC * nch * 16;
+  const int per_row = 8 * GC * L;  // threads per tile row
+  int TH = 256 / per_row;
+  if (TH < 1) return false;
+  const char* th_env = getenv("DCNV4_FWD33_TH");
+  if (th_env && *th_env) TH = std::max(1, std::min(TH, atoi(th_env)));
+  if (TH > Ho) TH = (int)Ho;
+  const int K = 9;
+  const int S = p->om_stride ? p->om_stride : 3 * p->G * K;
+  const int segB_raw = GC * 3 * K * b;
+  int unit = 0;
+  for (int u : {8, 4})
+    if ((S * b) % u == 0 && segB_raw % u == 0) { unit = u; break; }
+  if (!unit) return false;
+  int seg_bytes = (segB_raw + 15) & ~15;
+  if ((seg_bytes / 16) % 2 == 0) seg_bytes += 16;
+  const int HH = TH + 6, HWc = 14;
+  const int halo_box = HH * HWc * PB;
+  const int halo_bytes = (halo_box + 127) & ~127;
+  const size_t smem = 2 * (size_t)halo_bytes + 2 * (size_t)TH * 8 * seg_bytes + 16;
+  if (smem > 227 * 1024) return false;
+  const long long tiles_h = (Ho + TH - 1) / TH, tiles_w = (Wo + 7) / 8, gblocks = p->G / GC;
+  const long long tiles = (long long)p->N * tiles_h * tiles_w * gblocks;
+  if (tiles > 0x7fffffffLL) return false;
+  if (x == nullptr) return false;
+  if (reinterpret_cast<uintptr_t>(x) % 16) return false;
+  dcnv4::Launch l2 = *lc;
+  dcnv4::Geo g2 = *g;
+  if (!encode_x_map(p, dtype, x, GC * p->D, HWc, HH, &l2.xmap)) return false;
+  int shift;
+  conflict_factor(GC, L, cpl, nch, per_row * TH, &shift);
+  g2.TH = TH; g2.TW = 8; g2.Gc = GC;
+  g2.tiles_h = (int)tiles_h; g2.tiles_w = (int)tiles_w; g2.gblocks = (int)gblocks;
+  g2.tiles_total = (int)tiles;
+  g2.rot_shift = shift;
+  g2.seg = seg_bytes / b;
+  g2.HH = HH; g2.HW = HWc;
+  g2.halo_box_bytes = halo_box;
+  g2.halo_bytes = halo_bytes;
+  g2.unit = unit;
+  g2.upp = segB_raw / unit;
+  g2.fd_gb = make_fastdiv((unsigned)gblocks);
+  g2.fd_tw = make_fastdiv((unsigned)tiles_w);
+  g2.fd_th = make_fastdiv((unsigned)tiles_h);
+  g2.fd_upp = make_fastdiv((unsigned)g2.upp);
+  l2.halo = true;
+  l2.ppc = TH * 8;
+  l2.threads = per_row * TH;
+  l2.ctas = tiles;
+  l2.smem = smem;
+  *lc = l2;
+  *g = g2;
+  return true;
+}
+
+int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t Wo,
+                dcnv4::Launch* lc, dcnv4::Geo* g, const void* x = nullptr) {
   const int b = elem_size(dtype);
   const int nch = p->D * b / 16;
   int cpl = default_cpl(nch, pass);
@@ -115,32 +335,32 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
     int v = atoi(env);
     if (cpl_supported(nch, v)) cpl = v;
   }
-  // keep a pixel's G*lanes threads inside one CTA
-  while (p->G * (nch / cpl) > kMaxThreads && cpl < nch && cpl_supported(nch, cpl * 2)) cpl *= 2;
   const int lanes = nch / cpl;
-  const int gl = p->G * lanes;
-  if (gl > kMaxThreads)
-    return fail(DCNV4_ERR_UNSUPPORTED, "G*lanes = %d exceeds %d threads (G axis too large)", gl,
-                kMaxThreads);
   const int K = p->kernel_h * p->kernel_w;
   const int S = p->om_stride ? p->om_stride : 3 * p->G * K;
-  int ppc = kTargetThreads / gl;
-  if (ppc < 1) ppc = 1;
-  const long long P = (long long)p->N * Ho * Wo;
+  const TileChoice tc = choose_tile(p, b, nch, cpl, Ho, Wo, false);
+  const int npix = tc.TH * tc.TW;
+  // per-pixel om segment in shared memory: 16-B aligned, and an odd number of 16-B
+  // units so the rows of the <= 8 pixels a warp covers fall in distinct bank quads
+  int seg_bytes = ((tc.Gc * 3 * K * b) + 15) & ~15;
+  if ((seg_bytes / 16) % 2 == 0) seg_bytes += 16;
   lc->nch = nch;
   lc->cpl = cpl;
   lc->lanes = lanes;
-  lc->ppc = ppc;
-  lc->threads = ((ppc * gl + 31) / 32) * 32;
-  lc->ctas = (P + ppc - 1) / ppc;
-  size_t om_bytes = (((size_t)ppc * S * b + 16) + 15) & ~(size_t)15;
-  lc->smem = om_bytes + (pass == 1 ? (size_t)ppc * S * 4 : 0);
+  lc->ppc = npix;
+  lc->threads = ((npix * tc.Gc * lanes + 31) / 32) * 32;
+  const long long tiles_h = (Ho + tc.TH - 1) / tc.TH, tiles_w = (Wo + tc.TW - 1) / tc.TW;
+  lc->ctas = (long long)p->N * tiles_h * tiles_w * (p->G / tc.Gc);
+  lc->smem = (size_t)2 * npix * seg_bytes;  // double-buffered om tile
+  if (pass == 1) lc->smem = ((lc->smem + 15) & ~(size_t)15) + (size_t)npix * tc.Gc * 3 * K * sizeof(float);
   lc->k33 = p->kernel_h == 3 && p->kernel_w == 3;
   lc->unit = p->offset_scale == 1.0f;
+  if (lc->threads > kMaxThreads)
+    return fail(DCNV4_ERR_UNSUPPORTED, "CTA of %d threads exceeds %d", lc->threads, kMaxThreads);
   if (lc->smem > 227 * 1024)
     return fail(DCNV4_ERR_UNSUPPORTED, "offset_mask tile needs %zu B of shared memory", lc->smem);
   if (lc->ctas > 0x7fffffffLL)
-    return fail(DCNV4_ERR_SHAPE, "too many output pixels (N*Ho*Wo)");
+    return fail(DCNV4_ERR_SHAPE, "too many CTAs (N*Ho*Wo too large)");
   g->H = (int)p->H; g->W = (int)p->W; g->Ho = (int)Ho; g->Wo = (int)Wo;
   g->G = p->G; g->D = p->D; g->C = p->G * p->D; g->S = S; g->K = K;
   g->kh = p->kernel_h; g->kw = p->kernel_w; g->sh = p->stride_h; g->sw = p->stride_w;
@@ -149,8 +369,15 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
   g->cx = p->dilation_w * (p->kernel_w - 1) / 2;
   g->s = p->offset_scale;
   g->softmax = p->softmax;
-  g->P = P;
-  g->ppc = ppc;
+  g->TH = tc.TH; g->TW = tc.TW; g->Gc = tc.Gc;
+  g->tiles_h = (int)tiles_h; g->tiles_w = (int)tiles_w; g->gblocks = p->G / tc.Gc;
+  g->rot_shift = tc.rot_shift;
+  g->seg = seg_bytes / b;
+  lc->halo = false;
+  if (pass == 0) plan_fwd33(p, dtype, Ho, Wo, x, lc, g);
+  g->tiles_total = (int)lc->ctas;
+  const char* np = getenv("DCNV4_NONPERSISTENT");
+  lc->persistent = !(np && *np == '1');
   return DCNV4_OK;
 }
 
@@ -192,7 +419,7 @@ int dcnv4_launch_info(const dcnv4_params* p, dcnv4_dtype dtype, int pass, int32_
   if (rc) return rc;
   dcnv4::Launch lc;
   dcnv4::Geo g;
-  rc = make_launch(p, dtype, pass ? 1 : 0, Ho, Wo, &lc, &g);
+  rc = make_launch(p, dtype, pass ? 1 : 0, Ho, Wo, &lc, &g, reinterpret_cast<const void*>(256));
   if (rc) return rc;
   if (lanes) *lanes = lc.lanes;
   if (chunks_per_lane) *chunks_per_lane = lc.cpl;
@@ -218,7 +445,7 @@ int dcnv4_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input,
     return fail(DCNV4_ERR_MISALIGNED, "offset_mask is not element aligned");
   dcnv4::Launch lc;
   dcnv4::Geo g;
-  rc = make_launch(p, dtype, 0, Ho, Wo, &lc, &g);
+  rc = make_launch(p, dtype, 0, Ho, Wo, &lc, &g, input);
   if (rc) return rc;
   lc.stream = static_cast<cudaStream_t>(stream);
   cudaError_t e;

@@ -8,12 +8,37 @@
 
 namespace dcnv4 {
 
+// Persistent grid: as many CTAs as fit on the device at once (never more than tiles).
+static unsigned grid_size(const Launch& lc, const void* kern) {
+  if (!lc.persistent) return (unsigned)lc.ctas;
+  int dev = 0, sms = 148, per_sm = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, lc.threads, lc.smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const long long g = (long long)sms * per_sm;
+  return (unsigned)(g < lc.ctas ? g : lc.ctas);
+}
+
 template <typename T, int NCH, int CPL>
 static cudaError_t fwd_variant(const Launch& lc, const Geo& g, const void* x, const void* om,
                                void* y) {
   const T* xp = static_cast<const T*>(x);
   const T* op = static_cast<const T*>(om);
   T* yp = static_cast<T*>(y);
+  if (lc.halo) {  // 3x3 / stride 1 / dilation 1: TMA halo kernel
+    void (*hk)(const __grid_constant__ CUtensorMap, Geo, const T*, const T*, T*);
+    if (lc.unit) hk = fwd33_kernel<T, NCH, CPL, true>;
+    else hk = fwd33_kernel<T, NCH, CPL, false>;
+    if (lc.smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)lc.smem);
+      if (e != cudaSuccess) return e;
+    }
+    hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(lc.xmap, g, xp, op, yp);
+    return cudaGetLastError();
+  }
   void (*kern)(Geo, const T*, const T*, T*);
   if (lc.k33 && lc.unit) kern = fwd_kernel<T, NCH, CPL, 3, 3, true>;
   else if (lc.k33) kern = fwd_kernel<T, NCH, CPL, 3, 3, false>;
@@ -23,7 +48,7 @@ static cudaError_t fwd_variant(const Launch& lc, const Geo& g, const void* x, co
                                          (int)lc.smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<(unsigned)lc.ctas, lc.threads, lc.smem, lc.stream>>>(g, xp, op, yp);
+  kern<<<grid_size(lc, (const void*)kern), lc.threads, lc.smem, lc.stream>>>(g, xp, op, yp);
   return cudaGetLastError();
 }
 
@@ -43,7 +68,7 @@ static cudaError_t bwd_variant(const Launch& lc, const Geo& g, const void* x, co
                                          (int)lc.smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<(unsigned)lc.ctas, lc.threads, lc.smem, lc.stream>>>(g, xp, op, gyp, gx32, gomp);
+  kern<<<grid_size(lc, (const void*)kern), lc.threads, lc.smem, lc.stream>>>(g, xp, op, gyp, gx32, gomp);
   return cudaGetLastError();
 }
 

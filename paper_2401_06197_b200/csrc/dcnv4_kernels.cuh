@@ -8,9 +8,14 @@
 //     are read once per (pixel, group) from shared memory and the bilinear coefficients
 //     are computed once per (pixel, group, k) and reused across the lane's channels
 //     (P:318-324);
-//   * the CTA's offset_mask rows are one contiguous byte range; it is staged into
-//     shared memory with one TMA bulk copy (cp.async.bulk + mbarrier) -- the 16-B
-//     aligned body -- plus a few plain loads for the unaligned head/tail;
+//   * CTA = a 2-D tile of output pixels x a run of Gc groups of one image, so the
+//     CTA's corner footprint (tile + 7-pixel halo) stays L1-resident and x is fetched
+//     from L2 ~2-3x instead of ~17x (ncu, profiles/r01_v1_*);
+//   * persistent CTAs: the next tile's offset_mask segments are copied into a second
+//     shared-memory buffer with cp.async while the current tile is computed;
+//   * lanes are ordered (pixel, group, lane) and each lane's chunk order is rotated so
+//     the eight lanes of a 128-bit load phase hit eight distinct bank quads (microbench:
+//     115 vs 57-81 B/clk/SM, profiles/r01_microbench_l1_red.jsonl);
 //   * corner gathers are 16-byte read-only vector loads (LDG.E.128.CONSTANT), predicated
 //     off outside the image ("128-bit packed value");
 //   * fp32 accumulation for every storage type, RN-even store (P:329 half precision);
@@ -21,6 +26,7 @@
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,13 +34,30 @@ namespace dcnv4 {
 
 // Geometry handed to every kernel by value (validated on the host; per-image element
 // counts fit in int32).
+// Division by a runtime constant d for n < 2^31: q = (umulhi(n, m) + n) >> l
+// (m = ceil(2^(32+l)/d) - 2^32, l = ceil(log2 d); set up on the host).
+struct FastDiv {
+  unsigned m, l;
+};
+__device__ __forceinline__ unsigned fdiv(unsigned n, FastDiv f) { return (__umulhi(n, f.m) + n) >> f.l; }
+
 struct Geo {
   int H, W, Ho, Wo, G, D, C, S, K;
   int kh, kw, sh, sw, ph, pw, dh, dw, cy, cx;
   float s;
   int softmax;
-  long long P;  // N*Ho*Wo output pixels
-  int ppc;      // output pixels per CTA
+  // CTA tiling (chosen on the host, see dcnv4_api.cu make_launch)
+  int TH, TW, Gc;                  // output-pixel tile and groups per CTA
+  int tiles_h, tiles_w, gblocks;   // grid = N * tiles_h * tiles_w * gblocks
+  int rot_shift;                   // chunk-order stagger: rot = (pg_in_warp >> s) & (CPL-1)
+  int seg;                         // shared-memory elements per tile pixel (om segment)
+  int tiles_total;                 // N * tiles_h * tiles_w * gblocks (< 2^31)
+  // TMA halo path (forward): halo box = HH x HW pixels x Gc*D channels
+  int HH, HW;                      // halo rows / cols
+  int halo_bytes;                  // shared-memory bytes per halo buffer (128-B multiple)
+  int halo_box_bytes;              // bytes one TMA box delivers
+  int upp, unit;                   // om staging: units per tile pixel, unit bytes (8 or 4)
+  FastDiv fd_gb, fd_tw, fd_th, fd_upp;
 };
 
 // ------------------------------------------------------------------ element types
@@ -111,79 +134,153 @@ __device__ __forceinline__ uint4 ldg16(const void* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
 
+// 16-B read-only gather at base + idx*ES (one IMAD.WIDE.U32 for the address: idx is a
+// 32-bit element index inside one image, base a per-thread 64-bit pointer).
+template <int ES>
+__device__ __forceinline__ uint4 ldg16_idx(const void* base, unsigned idx) {
+  uint4 r;
+  asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %4, %6, %5;\n\t"
+      "ld.global.nc.v4.u32 {%0, %1, %2, %3}, [a];\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "r"(idx), "l"(base), "n"(ES));
+  return r;
+}
+
+// 16-B vector reduction into fp32 at base + idx*4.
+__device__ __forceinline__ void red_add_v4_idx(float* base, unsigned idx, float a, float b, float c,
+                                               float d) {
+  asm volatile("{\n\t.reg .u64 p;\n\tmad.wide.u32 p, %0, 4, %1;\n\t"
+               "red.global.add.v4.f32 [p], {%2, %3, %4, %5};\n\t}" ::"r"(idx), "l"(base), "f"(a),
+               "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b),
                "f"(c), "f"(d)
                : "memory");
 }
 
-// Stage `count` elements of T starting at global `src` into shared memory.  The 16-B
-// aligned body goes through one TMA bulk copy (UBLKCP) completing on an mbarrier; the
-// unaligned head/tail (< 16 B each) is copied by threads.  Returns the shared-memory
-// address of element 0.  Every thread of the CTA must call it.
-template <typename T>
-__device__ __forceinline__ const T* stage_rows(unsigned char* smem, uint64_t* bar,
-                                              const T* src, int count) {
-  const uintptr_t g0 = reinterpret_cast<uintptr_t>(src);
-  const uintptr_t g1 = g0 + (uintptr_t)count * sizeof(T);
-  const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15);
-  const uintptr_t a1 = g1 & ~uintptr_t(15);
-  const uintptr_t gbase = g0 & ~uintptr_t(15);          // maps to smem offset 0
-  T* tile = reinterpret_cast<T*>(smem + (g0 - gbase));
-  const bool bulk = a1 > a0;
-  if (threadIdx.x == 0 && bulk) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const uint32_t bytes = (uint32_t)(a1 - a0);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(smem + (a0 - gbase))),
-        "l"(a0), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-  }
-  // head [g0, min(a0, g1)) and tail [max(a1, a0), g1) by plain loads
-  const int head = bulk ? (int)((a0 - g0) / sizeof(T)) : count;
-  const int tail0 = bulk ? (int)((a1 - g0) / sizeof(T)) : count;
-  for (int e = threadIdx.x; e < head; e += blockDim.x) tile[e] = src[e];
-  for (int e = tail0 + threadIdx.x; e < count; e += blockDim.x) tile[e] = src[e];
-  __syncthreads();  // head/tail visible; mbarrier init visible to the waiters
-  if (bulk) {
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-          : "=r"(done)
-          : "r"(smem_u32(bar))
-          : "memory");
-    }
-  }
-  return tile;
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
 }
 
-// Sampling coordinate along one axis (R5, R11, R12):
-//   p = base + s*(tap + d),  i0 = floor(p),  f = p - i0.
-// With s == 1 the split is exact: floor and fraction of d alone, integer tap added
-// to the integer part.  Returns false (drop the sample) for NaN or |s*(tap+d)| > 2^20.
+// Asynchronous global -> shared copies (LDGSTS): the CTA's next offset_mask tile is
+// fetched while the current one is computed.
+template <int B>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+  if constexpr (B == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ------------------------------------------------------------------ tiles
+// A tile = one image n, a TH x TW block of output pixels and a run of Gc groups from g0.
+// Tile index = ((n * tiles_h + th) * tiles_w + tw) * gblocks + gb.  The grid is
+// persistent: CTA b processes tiles b, b + gridDim.x, ...
+struct Tile {
+  int n, h0, w0, g0;
+};
+
+__device__ __forceinline__ Tile decode_tile(const Geo& g, int t) {
+  Tile r;
+  const int gb = t % g.gblocks; t /= g.gblocks;
+  const int tw = t % g.tiles_w; t /= g.tiles_w;
+  const int th = t % g.tiles_h;
+  r.n = t / g.tiles_h;
+  r.h0 = th * g.TH;
+  r.w0 = tw * g.TW;
+  r.g0 = gb * g.Gc;
+  return r;
+}
+
+// Issue the copies of one tile's offset_mask rows into `buf`: per tile pixel the Gc*3K
+// contiguous values of groups [g0, g0+Gc), one segment per pixel (g.seg elements apart,
+// 16-B aligned).  One warp per pixel segment, widest unit the source alignment allows.
+template <typename T>
+__device__ __forceinline__ void stage_tile(const Geo& g, int t, const T* __restrict__ om,
+                                           T* buf) {
+  const Tile tl = decode_tile(g, t);
+  const int nbytes = g.Gc * 3 * g.K * (int)sizeof(T);
+  const int npix = g.TH * g.TW;
+  const int lane = threadIdx.x & 31;
+  for (int p = threadIdx.x >> 5; p < npix; p += blockDim.x >> 5) {
+    const int ho = tl.h0 + p / g.TW, wo = tl.w0 + p % g.TW;
+    if (ho >= g.Ho || wo >= g.Wo) continue;
+    const char* src = reinterpret_cast<const char*>(
+        om + ((long long)(tl.n * g.Ho + ho) * g.Wo + wo) * g.S + tl.g0 * 3 * g.K);
+    char* dst = reinterpret_cast<char*>(buf + p * g.seg);
+    const unsigned a = (unsigned)reinterpret_cast<uintptr_t>(src) | (unsigned)nbytes;
+    if ((a & 15) == 0) {
+      for (int i = lane * 16; i < nbytes; i += 512) cp_async<16>(dst + i, src + i);
+    } else if ((a & 7) == 0) {
+      for (int i = lane * 8; i < nbytes; i += 256) cp_async<8>(dst + i, src + i);
+    } else if ((a & 3) == 0) {
+      for (int i = lane * 4; i < nbytes; i += 128) cp_async<4>(dst + i, src + i);
+    } else {  // 2-byte aligned half rows: synchronous copy
+      const unsigned short* s2 = reinterpret_cast<const unsigned short*>(src);
+      unsigned short* d2 = reinterpret_cast<unsigned short*>(dst);
+      for (int i = lane; i < nbytes / 2; i += 32) d2[i] = s2[i];
+    }
+  }
+}
+
+// The bilinear sample of one point (R5-R7, R11, R12).  Coordinates are split
+// into an integer base and an fp32 fraction; with s == 1 the split is exact.  A NaN or
+// |s*(tap+d)| > 2^20 offset drops the sample.  Corner offsets are clamped into the image
+// so the four 16-B gathers are unconditional (no divergence, no register zeroing); an
+// out-of-image corner gets weight 0 and ok = false.
+struct Samp {
+  unsigned o[4]; // element offsets of the corners (image base excluded, group base included)
+  float w[4];    // bilinear weights, 0 for out-of-image corners
+  bool ok[4];    // corner inside the image
+  float fy, fx;  // fractional parts
+};
+
 template <bool UNIT>
-__device__ __forceinline__ bool locate(float s, int base, int tap, float d, int& i0, float& f) {
-  const float t = UNIT ? d : s * ((float)tap + d);
-  if (!(fabsf(t) <= 1048576.f)) return false;
-  const float fl = floorf(t);
-  f = t - fl;
-  i0 = base + (UNIT ? tap : 0) + (int)fl;
-  return true;
+__device__ __forceinline__ void sample(int H, int W, unsigned C, float s, int yb, int xb, int tapy,
+                                       int tapx, float dx, float dy, unsigned gbase, Samp& c) {
+  float ty = UNIT ? dy : s * ((float)tapy + dy);
+  float tx = UNIT ? dx : s * ((float)tapx + dx);
+  const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;  // false for NaN
+  ty = fin ? ty : 0.f;
+  tx = fin ? tx : 0.f;
+  const float fly = floorf(ty), flx = floorf(tx);
+  c.fy = ty - fly;
+  c.fx = tx - flx;
+  const int y0 = yb + (UNIT ? tapy : 0) + (int)fly;
+  const int x0 = xb + (UNIT ? tapx : 0) + (int)flx;
+  const bool vy0 = fin && (unsigned)y0 < (unsigned)H, vy1 = fin && (unsigned)(y0 + 1) < (unsigned)H;
+  const bool vx0 = (unsigned)x0 < (unsigned)W, vx1 = (unsigned)(x0 + 1) < (unsigned)W;
+  const int y0c = min(max(y0, 0), H - 1), y1c = min(max(y0 + 1, 0), H - 1);
+  const int x0c = min(max(x0, 0), W - 1), x1c = min(max(x0 + 1, 0), W - 1);
+  const unsigned r0 = (unsigned)(y0c * W), r1 = (unsigned)(y1c * W);
+  c.o[0] = (r0 + x0c) * C + gbase;
+  c.o[1] = (r0 + x1c) * C + gbase;
+  c.o[2] = (r1 + x0c) * C + gbase;
+  c.o[3] = (r1 + x1c) * C + gbase;
+  c.ok[0] = vy0 && vx0; c.ok[1] = vy0 && vx1; c.ok[2] = vy1 && vx0; c.ok[3] = vy1 && vx1;
+  const float hy = 1.f - c.fy, hx = 1.f - c.fx;
+  c.w[0] = c.ok[0] ? hy * hx : 0.f;
+  c.w[1] = c.ok[1] ? hy * c.fx : 0.f;
+  c.w[2] = c.ok[2] ? c.fy * hx : 0.f;
+  c.w[3] = c.ok[3] ? c.fy * c.fx : 0.f;
 }
 
 // The K modulation scalars of one (pixel, group): raw (DCNv4) or the softmax
 // over K (DCNv3; max-shifted).
 template <typename T, int KC>
-__device__ __forceinline__ void load_m(const T* row, int K, int softmax, float* m) {
+__device__ __forceinline__ void load_m(const T* row, int softmax, float* m) {
 #pragma unroll
-  for (int k = 0; k < KC; ++k) m[k] = Elem<T>::f(row[2 * K + k]);
+  for (int k = 0; k < KC; ++k) m[k] = Elem<T>::f(row[2 * KC + k]);
   if (softmax) {
     float mx = m[0];
 #pragma unroll
@@ -207,33 +304,29 @@ __device__ __forceinline__ void softmax_stats(const T* row, int K, float& mx, fl
   inv = 1.f / den;
 }
 
-// Bilinear corners of one sample: element offsets (relative to the image base, group
-// base already added) and weights; out-of-image corners get weight 0 and valid=false.
-struct Corners {
-  int off[4];
-  float w[4];
-  bool ok[4];
-  float fy, fx;
+// Per-thread slot inside every tile (the tile shape is fixed for the launch): threads
+// are ordered (pixel, group, lane) -- lane fastest, then group, then pixel (x fastest) --
+// so a warp covers consecutive groups of neighbouring pixels.  The lane's 16-B chunks are
+// dealt round-robin over the L lanes (L x 16 B contiguous per instruction) and their order
+// is rotated so an 8-lane phase of a 128-bit load touches 8 distinct bank quads
+// (microbench: 115 vs 57-81 B/clk/SM, profiles/r01_microbench_l1_red.jsonl).
+template <int L, int CPL, int E>
+struct Slot {
+  int p, py, px, gl, lg;
+  int co[CPL];  // element offset of the lane's h-th chunk inside the group vector
+  __device__ __forceinline__ Slot(const Geo& g) {
+    const int t = threadIdx.x;
+    lg = t % L;
+    const int q = t / L;
+    gl = q % g.Gc;
+    p = q / g.Gc;
+    py = p / g.TW;
+    px = p - py * g.TW;
+    const int rot = g.rot_shift < 0 ? 0 : (((t & 31) / L) >> g.rot_shift) & (CPL - 1);
+#pragma unroll
+    for (int h = 0; h < CPL; ++h) co[h] = (((h + rot) & (CPL - 1)) * L + lg) * E;
+  }
 };
-
-template <bool UNIT>
-__device__ __forceinline__ void corners(const Geo& g, int yb, int xb, int tapy, int tapx,
-                                        float dx, float dy, int gbase, Corners& c) {
-  int y0, x0;
-  float fy, fx;
-  const bool oky = locate<UNIT>(g.s, yb, tapy, dy, y0, fy);
-  const bool okx = locate<UNIT>(g.s, xb, tapx, dx, x0, fx);
-  const bool ok = oky && okx;
-  if (!ok) { y0 = -2; x0 = -2; fy = 0.f; fx = 0.f; }
-  const bool vy0 = (unsigned)y0 < (unsigned)g.H, vy1 = (unsigned)(y0 + 1) < (unsigned)g.H;
-  const bool vx0 = (unsigned)x0 < (unsigned)g.W, vx1 = (unsigned)(x0 + 1) < (unsigned)g.W;
-  const float hy = 1.f - fy, hx = 1.f - fx;
-  c.fy = fy; c.fx = fx;
-  c.w[0] = hy * hx; c.w[1] = hy * fx; c.w[2] = fy * hx; c.w[3] = fy * fx;
-  c.ok[0] = vy0 && vx0; c.ok[1] = vy0 && vx1; c.ok[2] = vy1 && vx0; c.ok[3] = vy1 && vx1;
-  const int o = (y0 * g.W + x0) * g.C + gbase;
-  c.off[0] = o; c.off[1] = o + g.C; c.off[2] = o + g.W * g.C; c.off[3] = o + g.W * g.C + g.C;
-}
 
 // ------------------------------------------------------------------ forward
 // KH = KW = 0: runtime kernel size; otherwise compile-time (3x3 is the paper's grid).
@@ -245,81 +338,335 @@ __global__ void __launch_bounds__(256) fwd_kernel(Geo g, const T* __restrict__ x
   constexpr int E = Elem<T>::E;
   constexpr int KC = KH * KW;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint64_t bar;
+  T* const bufs0 = reinterpret_cast<T*>(smem);
+  const int bstride = g.TH * g.TW * g.seg;
+  const Slot<L, CPL, E> sl(g);
+  const bool slot_ok = sl.p < g.TH * g.TW;
+  const int H = g.H, W = g.W, C = g.C, K = KC ? KC : g.K;
+  const float s = g.s;
 
-  const long long p_first = (long long)blockIdx.x * g.ppc;
-  const int npix = (int)min((long long)g.ppc, g.P - p_first);
-  const T* tile = stage_rows<T>(smem, &bar, om + p_first * g.S, npix * g.S);
-
-  const int GL = g.G * L;
-  const int t = threadIdx.x;
-  const int pl = t / GL;
-  if (pl >= npix) return;
-  const int rem = t - pl * GL;
-  const int grp = rem / L;
-  const int lg = rem - grp * L;
-  const long long pix = p_first + pl;
-  const int HWo = g.Ho * g.Wo;
-  const int n = (int)(pix / HWo);
-  const int hw = (int)(pix - (long long)n * HWo);
-  const int ho = hw / g.Wo, wo = hw - (hw / g.Wo) * g.Wo;
-  const int yb = ho * g.sh - g.ph + g.cy;
-  const int xb = wo * g.sw - g.pw + g.cx;
-  const T* ximg = x + (long long)n * g.H * g.W * g.C;
-  const int K = KC ? KC : g.K;
-  const T* row = tile + pl * g.S + grp * 3 * K;
-  const int cbase = grp * g.D + lg * CPL * E;
-
-  float acc[CPL * E];
+  int t = blockIdx.x;
+  stage_tile<T>(g, t, om, bufs0);
+  cp_async_commit();
+  for (int it = 0; t < g.tiles_total; t += gridDim.x, ++it) {
+    const int tn = t + gridDim.x;
+    if (tn < g.tiles_total) stage_tile<T>(g, tn, om, bufs0 + ((it + 1) & 1) * bstride);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const Tile tl = decode_tile(g, t);
+    const int ho = tl.h0 + sl.py, wo = tl.w0 + sl.px;
+    if (slot_ok && ho < g.Ho && wo < g.Wo) {
+      const T* row = bufs0 + (it & 1) * bstride + sl.p * g.seg + sl.gl * 3 * K;
+      const int grp = tl.g0 + sl.gl;
+      const unsigned gbase = grp * g.D;
+      const int yb = ho * g.sh - g.ph + g.cy;
+      const int xb = wo * g.sw - g.pw + g.cx;
+      const T* ximg = x + (long long)tl.n * H * W * C;
+      const T* xh[CPL];  // per-chunk base pointers: one IMAD.WIDE per gather address
 #pragma unroll
-  for (int e = 0; e < CPL * E; ++e) acc[e] = 0.f;
-
-  auto do_point = [&](int i, int j, int k, float m) {
-    Corners c;
-    corners<UNIT>(g, yb, xb, j * g.dh - g.cy, i * g.dw - g.cx, Elem<T>::f(row[2 * k]),
-                  Elem<T>::f(row[2 * k + 1]), cbase, c);
+      for (int h = 0; h < CPL; ++h) xh[h] = ximg + sl.co[h];
+      float acc[CPL * E];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float a = c.ok[q] ? m * c.w[q] : 0.f;
+      for (int e = 0; e < CPL * E; ++e) acc[e] = 0.f;
+      auto point = [&](int i, int j, int k, float m) {
+        Samp c;
+        sample<UNIT>(H, W, C, s, yb, xb, j * g.dh - g.cy, i * g.dw - g.cx,
+                     Elem<T>::f(row[2 * k]), Elem<T>::f(row[2 * k + 1]), gbase, c);
+        uint4 u[4][CPL];
 #pragma unroll
-      for (int h = 0; h < CPL; ++h) {
-        uint4 u = make_uint4(0, 0, 0, 0);
-        if (c.ok[q]) u = ldg16(ximg + c.off[q] + h * E);
-        float v[E];
-        Elem<T>::unpack(u, v);
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc[h * E + e] = fmaf(a, v[e], acc[h * E + e]);
+          for (int h = 0; h < CPL; ++h) u[q][h] = ldg16_idx<sizeof(T)>(xh[h], c.o[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float a = m * c.w[q];
+#pragma unroll
+          for (int h = 0; h < CPL; ++h) {
+            float v[E];
+            Elem<T>::unpack(u[q][h], v);
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[h * E + e] = fmaf(a, v[e], acc[h * E + e]);
+          }
+        }
+      };
+      if constexpr (KC > 0) {
+        float m[KC];
+        load_m<T, KC>(row, g.softmax, m);
+#pragma unroll
+        for (int i = 0; i < KW; ++i)
+#pragma unroll
+          for (int j = 0; j < KH; ++j) point(i, j, i * KH + j, m[i * KH + j]);
+      } else {
+        float mx = 0.f, inv = 1.f;
+        if (g.softmax) softmax_stats<T>(row, K, mx, inv);
+        for (int i = 0; i < g.kw; ++i)
+          for (int j = 0; j < g.kh; ++j) {
+            const int k = i * g.kh + j;
+            float m = Elem<T>::f(row[2 * K + k]);
+            if (g.softmax) m = __expf(m - mx) * inv;
+            point(i, j, k, m);
+          }
       }
+      T* yo = y + ((long long)(tl.n * g.Ho + ho) * g.Wo + wo) * C + gbase;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h)
+        *reinterpret_cast<uint4*>(yo + sl.co[h]) = Elem<T>::pack(acc + h * E);
+    }
+    __syncthreads();  // everyone is done with bufs[it & 1] before it is refilled
+  }
+  cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------ forward, TMA halo path
+// The CTA's input footprint -- the tile plus a 2-pixel margin around the conv window,
+// HH x HW pixels x Gc*D channels -- is fetched into shared memory by ONE TMA tensor
+// copy (cp.async.bulk.tensor.4d, UTMALDG) that also zero-fills out-of-image pixels, so
+// in-halo samples need no bounds checks, no clamping and only 32-bit shared addresses.
+// Samples that leave the halo (|offset| >= 2 px) are recorded in a bit mask and added
+// after the main loop with bounds-checked global gathers (rare; the main loop is
+// branch-free).
+// Halo and offset_mask tiles are double-buffered: the next tile's copies are in flight
+// while the current tile is computed (persistent CTAs).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+          "r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds16(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+  return r;
+}
+
+// acc[0..E) += a * v (fp32 pairs through FFMA2)
+template <int E>
+__device__ __forceinline__ void axpy2(float* acc, float a, const float* v) {
+  const float2 a2 = make_float2(a, a);
+#pragma unroll
+  for (int e = 0; e < E; e += 2) {
+    float2 r = __ffma2_rn(a2, make_float2(v[e], v[e + 1]), make_float2(acc[e], acc[e + 1]));
+    acc[e] = r.x;
+    acc[e + 1] = r.y;
+  }
+}
+
+template <typename T, int NCH, int CPL, bool UNIT>
+__global__ void __launch_bounds__(256) fwd33_kernel(const __grid_constant__ CUtensorMap xmap, Geo g,
+                                                    const T* __restrict__ x,
+                                                    const T* __restrict__ om,
+                                                    T* __restrict__ y) {
+  // Specialised for the paper's grid (3x3, stride 1, dilation 1; any padding):
+  //   TW = 8 output columns, GC groups per CTA so one halo pixel is PB = GC*D*b >= 128 B,
+  //   halo = (TH + 6) x 14 pixels, all strides compile-time (shift/immediate addressing).
+  constexpr int L = NCH / CPL;
+  constexpr int E = Elem<T>::E;
+  constexpr int GC = NCH >= 8 ? 1 : 8 / NCH;
+  constexpr int PB = GC * NCH * 16;
+  constexpr int TW = 8, HWC = TW + 6, ROWB = HWC * PB;
+  constexpr int K = 9;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int TH = g.TH, HH = TH + 6;
+  const int npix = TH * TW;
+  T* const ombase = reinterpret_cast<T*>(smem + 2 * g.halo_bytes);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(
+      smem + 2 * g.halo_bytes + ((2 * npix * g.seg * (int)sizeof(T) + 7) & ~7));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // thread slot: (pixel row, pixel col, group, lane) -- all powers of two
+  const int tid = threadIdx.x;
+  const int lg = tid % L;
+  const int gl = (tid / L) % GC;
+  const int px = (tid / (L * GC)) % TW;
+  const int py = tid / (L * GC * TW);
+  const bool slot_ok = py < TH;
+  const int rot = g.rot_shift < 0 ? 0 : (((tid & 31) / L) >> g.rot_shift) & (CPL - 1);
+  int co[CPL];
+  uint32_t hb0[CPL];
+#pragma unroll
+  for (int h = 0; h < CPL; ++h) {
+    co[h] = (((h + rot) & (CPL - 1)) * L + lg) * E;
+    hb0[h] = smem_u32(smem) + (uint32_t)(gl * NCH * 16 + co[h] * (int)sizeof(T));
+  }
+  const int H = g.H, W = g.W, C = g.C;
+  const float s = g.s;
+  const unsigned segB = (unsigned)g.seg * sizeof(T);
+
+  auto decode = [&](int t, int& n, int& h0, int& w0, int& g0) {
+    const unsigned q1 = fdiv((unsigned)t, g.fd_gb);
+    g0 = (t - (int)q1 * g.gblocks) * GC;
+    const unsigned q2 = fdiv(q1, g.fd_tw);
+    w0 = ((int)q1 - (int)q2 * g.tiles_w) * TW;
+    const unsigned q3 = fdiv(q2, g.fd_th);
+    h0 = ((int)q2 - (int)q3 * g.tiles_h) * TH;
+    n = (int)q3;
+  };
+  auto issue = [&](int t, int b) {
+    int n, h0, w0, g0;
+    decode(t, n, h0, w0, g0);
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bar[b], (uint32_t)g.halo_box_bytes);
+      tma_load_4d(smem + b * g.halo_bytes, &xmap, g0 * g.D, w0 - g.pw - 2, h0 - g.ph - 2, n, &bar[b]);
+    }
+    // offset_mask: GC*3K values per tile pixel, as upp units of g.unit bytes
+    const char* src0 = reinterpret_cast<const char*>(
+        om + ((long long)(n * g.Ho + h0) * g.Wo + w0) * g.S + g0 * 3 * K);
+    unsigned char* dst0 = reinterpret_cast<unsigned char*>(ombase + b * npix * g.seg);
+    const unsigned rowS = (unsigned)g.Wo * g.S * sizeof(T), pixS = (unsigned)g.S * sizeof(T);
+    for (int f = tid; f < npix * g.upp; f += blockDim.x) {
+      const int pix = (int)fdiv((unsigned)f, g.fd_upp);
+      const int u = f - pix * g.upp;
+      const int ppy = pix / TW, ppx = pix % TW;
+      if (h0 + ppy >= g.Ho || w0 + ppx >= g.Wo) continue;
+      const char* src = src0 + (ppy * rowS + ppx * pixS + (unsigned)(u * g.unit));
+      unsigned char* dst = dst0 + pix * segB + u * g.unit;
+      if (g.unit == 8) cp_async<8>(dst, src);
+      else cp_async<4>(dst, src);
     }
   };
 
-  if constexpr (KC > 0) {
-    float m[KC];
-    load_m<T, KC>(row, KC, g.softmax, m);
+  int t = blockIdx.x;
+  issue(t, 0);
+  cp_async_commit();
+  for (int it = 0; t < g.tiles_total; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int tn = t + gridDim.x;
+    if (tn < g.tiles_total) issue(tn, b ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    mbar_wait(&bar[b], (uint32_t)((it >> 1) & 1));
+    __syncthreads();
+    int n, h0, w0, g0;
+    decode(t, n, h0, w0, g0);
+    const int ho = h0 + py, wo = w0 + px;
+    if (slot_ok && ho < g.Ho && wo < g.Wo) {
+      const T* row = ombase + b * npix * g.seg + (py * TW + px) * g.seg + gl * 3 * K;
+      const unsigned gbase = (g0 + gl) * g.D;
+      uint32_t hb[CPL];
 #pragma unroll
-    for (int i = 0; i < KW; ++i)
+      for (int h = 0; h < CPL; ++h) hb[h] = hb0[h] + (uint32_t)(b * g.halo_bytes);
+      float m[K];
+      load_m<T, K>(row, g.softmax, m);
+      float acc[CPL * E];
 #pragma unroll
-      for (int j = 0; j < KH; ++j) do_point(i, j, i * KH + j, m[i * KH + j]);
-  } else {
-    float mx = 0.f, inv = 1.f;
-    if (g.softmax) softmax_stats<T>(row, K, mx, inv);
-    for (int i = 0; i < g.kw; ++i)
-      for (int j = 0; j < g.kh; ++j) {
-        const int k = i * g.kh + j;
-        float m = Elem<T>::f(row[2 * K + k]);
-        if (g.softmax) m = __expf(m - mx) * inv;
-        do_point(i, j, k, m);
+      for (int e = 0; e < CPL * E; ++e) acc[e] = 0.f;
+      unsigned outside = 0;  // samples that left the halo (handled after the main loop)
+      struct Fetched {
+        uint4 u[4][CPL];
+        float a[4];
+      };
+      auto fetch = [&](int k, Fetched& F) {
+        const int i = k / 3, j = k % 3;
+        const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
+        float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
+        float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
+        const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
+        ty = fin ? ty : 0.f;
+        tx = fin ? tx : 0.f;
+        const float fly = floorf(ty), flx = floorf(tx);
+        const float fy = ty - fly, fx = tx - flx;
+        // local halo coordinates: halo origin = (h0 - ph - 2, w0 - pw - 2)
+        const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
+        const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
+        const bool in = (unsigned)yl <= (unsigned)(HH - 2) && (unsigned)xl <= (unsigned)(HWC - 2);
+        outside |= (fin && !in) ? (1u << k) : 0u;
+        const float mk = (fin && in) ? m[k] : 0.f;
+        const uint32_t off = (uint32_t)((in ? yl : 0) * ROWB + (in ? xl : 0) * PB);
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) {
+          const uint32_t a0 = hb[h] + off;
+          F.u[0][h] = lds16(a0);
+          F.u[1][h] = lds16(a0 + PB);
+          F.u[2][h] = lds16(a0 + ROWB);
+          F.u[3][h] = lds16(a0 + ROWB + PB);
+        }
+        const float my = mk * (1.f - fy), ny = mk * fy;
+        F.a[0] = my * (1.f - fx); F.a[1] = my * fx; F.a[2] = ny * (1.f - fx); F.a[3] = ny * fx;
+      };
+      auto accum = [&](const Fetched& F) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < CPL; ++h) {
+            float v[E];
+            Elem<T>::unpack(F.u[q][h], v);
+            axpy2<E>(acc + h * E, F.a[q], v);
+          }
+      };
+      // software pipeline: the gathers of point k+1 are issued before the FMAs of k
+      Fetched F0, F1;
+      fetch(0, F0);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (k + 1 < K) fetch(k + 1, (k & 1) ? F0 : F1);
+        accum((k & 1) ? F1 : F0);
       }
-  }
-
-  T* yo = y + pix * g.C + cbase;
+      if (outside) {  // rare: |offset| >= 2 px -- bounds-checked global gathers
+        const T* ximg = x + (long long)n * H * W * C;
+        float smx = 0.f, sinv = 1.f;
+        if (g.softmax) softmax_stats<T>(row, K, smx, sinv);
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+          if (!((outside >> k) & 1u)) continue;
+          float mk = Elem<T>::f(row[2 * K + k]);  // re-read: m[] must stay in registers
+          if (g.softmax) mk = __expf(mk - smx) * sinv;
+          const int i = k / 3, j = k % 3;
+          Samp c;
+          sample<UNIT>(H, W, C, s, ho - g.ph + 1, wo - g.pw + 1, j - 1, i - 1,
+                       Elem<T>::f(row[2 * k]), Elem<T>::f(row[2 * k + 1]), gbase, c);
 #pragma unroll
-  for (int h = 0; h < CPL; ++h)
-    *reinterpret_cast<uint4*>(yo + h * E) = Elem<T>::pack(acc + h * E);
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int h = 0; h < CPL; ++h) {
+              float v[E];
+              Elem<T>::unpack(ldg16_idx<sizeof(T)>(ximg + co[h], c.o[q]), v);
+              axpy2<E>(acc + h * E, mk * c.w[q], v);
+            }
+        }
+      }
+      T* yo = y + ((long long)(n * g.Ho + ho) * g.Wo + wo) * C + gbase;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h)
+        *reinterpret_cast<uint4*>(yo + co[h]) = Elem<T>::pack(acc + h * E);
+    }
+    __syncthreads();  // everyone is done with halo[b] / om[b] before they are refilled
+  }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ backward
 // gx32: fp32 accumulator [N][H][W][C], zeroed by the host before launch.
+// Per (pixel, group, k) with corner vectors v_q and this lane's gy:
+//   S_q = sum_c gy_c v_qc          (4 dot products, the only per-channel work)
+//   grad_m  partial = sum_q w_q S_q
+//   grad_dy partial = (1-fx)(S_2 - S_0) + fx (S_3 - S_1)     [times s*m]
+//   grad_dx partial = (1-fy)(S_1 - S_0) + fy (S_3 - S_2)     [times s*m]
+// (S_q of out-of-image corners is 0) reduced over the L lanes with shuffles;
+// grad_input += m w_q gy by 16-B vector reductions.
 template <typename T, int NCH, int CPL, int KH, int KW, bool UNIT>
 __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x,
                                                   const T* __restrict__ om,
@@ -330,139 +677,153 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x
   constexpr int E = Elem<T>::E;
   constexpr int KC = KH * KW;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint64_t bar;
-
-  const long long p_first = (long long)blockIdx.x * g.ppc;
-  const int npix = (int)min((long long)g.ppc, g.P - p_first);
-  // shared memory: [om tile (+16 B slack)] [fp32 grad tile, ppc*S]
-  const int om_bytes = ((g.ppc * g.S * (int)sizeof(T) + 16) + 15) & ~15;
-  float* gtile = reinterpret_cast<float*>(smem + om_bytes);
-  for (int e = threadIdx.x; e < npix * g.S; e += blockDim.x) gtile[e] = 0.f;
-  const T* tile = stage_rows<T>(smem, &bar, om + p_first * g.S, npix * g.S);
-
-  const int GL = g.G * L;
-  const int t = threadIdx.x;
-  const int pl0 = t / GL;
-  const bool active = pl0 < npix;  // inactive lanes still take part in the shuffles
-  const int pl = active ? pl0 : 0;
-  const int rem = t - pl0 * GL;
-  const int grp = rem / L;
-  const int lg = rem - grp * L;
-  const long long pix = p_first + pl;
-  const int HWo = g.Ho * g.Wo;
-  const int n = (int)(pix / HWo);
-  const int hw = (int)(pix - (long long)n * HWo);
-  const int ho = hw / g.Wo, wo = hw - (hw / g.Wo) * g.Wo;
-  const int yb = ho * g.sh - g.ph + g.cy;
-  const int xb = wo * g.sw - g.pw + g.cx;
-  const long long img = (long long)n * g.H * g.W * g.C;
-  const T* ximg = x + img;
-  float* gximg = gx32 + img;
+  const int npix = g.TH * g.TW;
+  T* const bufs0 = reinterpret_cast<T*>(smem);
+  const int bstride = npix * g.seg;
   const int K = KC ? KC : g.K;
-  const T* row = tile + pl * g.S + grp * 3 * K;
-  float* grow = gtile + pl * g.S + grp * 3 * K;
-  const int cbase = grp * g.D + lg * CPL * E;
+  const int seg32 = g.Gc * 3 * K;
+  float* gtile = reinterpret_cast<float*>(smem + (((size_t)2 * npix * g.seg * sizeof(T) + 15) & ~(size_t)15));
+  const Slot<L, CPL, E> sl(g);
+  const bool slot_ok = sl.p < npix;
+  const int H = g.H, W = g.W, C = g.C;
+  const float s = g.s;
+  const int lane = threadIdx.x & 31;
 
-  float gyv[CPL * E];
-  {
-    const T* gyo = gy + pix * g.C + cbase;
+  int t = blockIdx.x;
+  stage_tile<T>(g, t, om, bufs0);
+  cp_async_commit();
+  for (int it = 0; t < g.tiles_total; t += gridDim.x, ++it) {
+    const int tn = t + gridDim.x;
+    if (tn < g.tiles_total) stage_tile<T>(g, tn, om, bufs0 + ((it + 1) & 1) * bstride);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const Tile tl = decode_tile(g, t);
+    const int ho0 = tl.h0 + sl.py, wo0 = tl.w0 + sl.px;
+    const bool active = slot_ok && ho0 < g.Ho && wo0 < g.Wo;  // inactive lanes still shuffle
+    const int ho = active ? ho0 : tl.h0, wo = active ? wo0 : tl.w0;
+    const int pp = active ? sl.p : 0;
+    const T* row = bufs0 + (it & 1) * bstride + pp * g.seg + sl.gl * 3 * K;
+    float* grow = gtile + pp * seg32 + sl.gl * 3 * K;
+    const int grp = tl.g0 + sl.gl;
+    const unsigned gbase = grp * g.D;
+    const int yb = ho * g.sh - g.ph + g.cy;
+    const int xb = wo * g.sw - g.pw + g.cx;
+    const long long img = (long long)tl.n * H * W * C;
+    const T* xh[CPL];
+    float* gxh[CPL];
 #pragma unroll
-    for (int h = 0; h < CPL; ++h) {
-      uint4 u = make_uint4(0, 0, 0, 0);
-      if (active) u = ldg16(gyo + h * E);
-      Elem<T>::unpack(u, gyv + h * E);
+    for (int h = 0; h < CPL; ++h) { xh[h] = x + img + sl.co[h]; gxh[h] = gx32 + img + sl.co[h]; }
+
+    float gyv[CPL * E];
+    {
+      const T* gyo = gy + ((long long)(tl.n * g.Ho + ho) * g.Wo + wo) * C + gbase;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        uint4 u = ld_stream(reinterpret_cast<const uint4*>(gyo + sl.co[h]));
+        Elem<T>::unpack(u, gyv + h * E);
+      }
     }
-  }
 
-  auto do_point = [&](int i, int j, int k, float m) {
-    Corners c;
-    corners<UNIT>(g, yb, xb, j * g.dh - g.cy, i * g.dw - g.cx, Elem<T>::f(row[2 * k]),
-                  Elem<T>::f(row[2 * k + 1]), cbase, c);
-    float sgm = 0.f, sgy = 0.f, sgx = 0.f;
-    const float hy = 1.f - c.fy, hx = 1.f - c.fx;
+    auto point = [&](int i, int j, int k, float m) {
+      Samp c;
+      sample<UNIT>(H, W, C, s, yb, xb, j * g.dh - g.cy, i * g.dw - g.cx,
+                   Elem<T>::f(row[2 * k]), Elem<T>::f(row[2 * k + 1]), gbase, c);
+      uint4 u[4][CPL];
 #pragma unroll
-    for (int h = 0; h < CPL; ++h) {
-      float v[4][E];
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 u = make_uint4(0, 0, 0, 0);
-        if (active && c.ok[q]) u = ldg16(ximg + c.off[q] + h * E);
-        Elem<T>::unpack(u, v[q]);
-      }
+        for (int h = 0; h < CPL; ++h) u[q][h] = ldg16_idx<sizeof(T)>(xh[h], c.o[q]);
+      float S[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const float gye = gyv[h * E + e];
-        const float val = c.w[0] * v[0][e] + c.w[1] * v[1][e] + c.w[2] * v[2][e] + c.w[3] * v[3][e];
-        const float dvy = hx * (v[2][e] - v[0][e]) + c.fx * (v[3][e] - v[1][e]);
-        const float dvx = hy * (v[1][e] - v[0][e]) + c.fy * (v[3][e] - v[2][e]);
-        sgm = fmaf(gye, val, sgm);
-        sgy = fmaf(gye, dvy, sgy);
-        sgx = fmaf(gye, dvx, sgx);
-      }
-      // bilinear scatter of m*w*gy into the in-bounds corners
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) {
+          float v[E];
+          Elem<T>::unpack(u[q][h], v);
+#pragma unroll
+          for (int e = 0; e < E; ++e) S[q] = fmaf(gyv[h * E + e], v[e], S[q]);
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) S[q] = (active && c.ok[q]) ? S[q] : 0.f;
+      // bilinear scatter of m*w*gy into the in-image corners
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (active && c.ok[q]) {
-          const float a = m * c.w[q];
-          float* dst = gximg + c.off[q] + h * E;
+        const float a = m * c.w[q];
+        if (active && a != 0.f) {
 #pragma unroll
-          for (int e = 0; e < E; e += 4)
-            red_add_v4(dst + e, a * gyv[h * E + e], a * gyv[h * E + e + 1],
-                       a * gyv[h * E + e + 2], a * gyv[h * E + e + 3]);
+          for (int h = 0; h < CPL; ++h) {
+#pragma unroll
+            for (int e = 0; e < E; e += 4)
+              red_add_v4_idx(gxh[h] + e, c.o[q], a * gyv[h * E + e], a * gyv[h * E + e + 1],
+                             a * gyv[h * E + e + 2], a * gyv[h * E + e + 3]);
+          }
+        }
+      }
+      const float hy = 1.f - c.fy, hx = 1.f - c.fx;
+      float sgm = c.w[0] * S[0] + c.w[1] * S[1] + c.w[2] * S[2] + c.w[3] * S[3];
+      float sgy = hx * (S[2] - S[0]) + c.fx * (S[3] - S[1]);
+      float sgx = hy * (S[1] - S[0]) + c.fy * (S[3] - S[2]);
+#pragma unroll
+      for (int o = 1; o < L; o <<= 1) {
+        sgm += __shfl_xor_sync(0xffffffffu, sgm, o);
+        sgy += __shfl_xor_sync(0xffffffffu, sgy, o);
+        sgx += __shfl_xor_sync(0xffffffffu, sgx, o);
+      }
+      if (active && sl.lg == 0) {
+        grow[2 * k] = s * m * sgx;      // d/d dx_k
+        grow[2 * k + 1] = s * m * sgy;  // d/d dy_k
+        grow[2 * K + k] = sgm;          // d/d m_k
+      }
+    };
+
+    if constexpr (KC > 0) {
+      float m[KC];
+      load_m<T, KC>(row, g.softmax, m);
+#pragma unroll
+      for (int i = 0; i < KW; ++i)
+#pragma unroll
+        for (int j = 0; j < KH; ++j) point(i, j, i * KH + j, m[i * KH + j]);
+      if (g.softmax && active && sl.lg == 0) {  // dL/dz_k = p_k (gm_k - sum_j p_j gm_j)
+        float dot = 0.f;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) dot += m[k] * grow[2 * KC + k];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) grow[2 * KC + k] = m[k] * (grow[2 * KC + k] - dot);
+      }
+    } else {
+      float mx = 0.f, inv = 1.f;
+      if (g.softmax) softmax_stats<T>(row, K, mx, inv);
+      for (int i = 0; i < g.kw; ++i)
+        for (int j = 0; j < g.kh; ++j) {
+          const int k = i * g.kh + j;
+          float m = Elem<T>::f(row[2 * K + k]);
+          if (g.softmax) m = __expf(m - mx) * inv;
+          point(i, j, k, m);
+        }
+      if (g.softmax && active && sl.lg == 0) {
+        float dot = 0.f;
+        for (int k = 0; k < K; ++k) dot += __expf(Elem<T>::f(row[2 * K + k]) - mx) * inv * grow[2 * K + k];
+        for (int k = 0; k < K; ++k) {
+          const float p = __expf(Elem<T>::f(row[2 * K + k]) - mx) * inv;
+          grow[2 * K + k] = p * (grow[2 * K + k] - dot);
         }
       }
     }
-    // reduce the three partial dot products over the L lanes of this (pixel, group)
-#pragma unroll
-    for (int o = 1; o < L; o <<= 1) {
-      sgm += __shfl_xor_sync(0xffffffffu, sgm, o);
-      sgy += __shfl_xor_sync(0xffffffffu, sgy, o);
-      sgx += __shfl_xor_sync(0xffffffffu, sgx, o);
-    }
-    if (active && lg == 0) {
-      grow[2 * k] = g.s * m * sgx;      // d/d dx_k
-      grow[2 * k + 1] = g.s * m * sgy;  // d/d dy_k
-      grow[2 * K + k] = sgm;            // d/d m_k
-    }
-  };
-
-  if constexpr (KC > 0) {
-    float m[KC];
-    load_m<T, KC>(row, KC, g.softmax, m);
-#pragma unroll
-    for (int i = 0; i < KW; ++i)
-#pragma unroll
-      for (int j = 0; j < KH; ++j) do_point(i, j, i * KH + j, m[i * KH + j]);
-    if (g.softmax && active && lg == 0) {  // dL/dz_k = p_k (gm_k - sum_j p_j gm_j)
-      float dot = 0.f;
-#pragma unroll
-      for (int k = 0; k < KC; ++k) dot += m[k] * grow[2 * KC + k];
-#pragma unroll
-      for (int k = 0; k < KC; ++k) grow[2 * KC + k] = m[k] * (grow[2 * KC + k] - dot);
-    }
-  } else {
-    float mx = 0.f, inv = 1.f;
-    if (g.softmax) softmax_stats<T>(row, K, mx, inv);
-    for (int i = 0; i < g.kw; ++i)
-      for (int j = 0; j < g.kh; ++j) {
-        const int k = i * g.kh + j;
-        float m = Elem<T>::f(row[2 * K + k]);
-        if (g.softmax) m = __expf(m - mx) * inv;
-        do_point(i, j, k, m);
-      }
-    if (g.softmax && active && lg == 0) {
-      float dot = 0.f;
-      for (int k = 0; k < K; ++k) dot += __expf(Elem<T>::f(row[2 * K + k]) - mx) * inv * grow[2 * K + k];
-      for (int k = 0; k < K; ++k) {
-        const float p = __expf(Elem<T>::f(row[2 * K + k]) - mx) * inv;
-        grow[2 * K + k] = p * (grow[2 * K + k] - dot);
-      }
+    __syncthreads();
+    // write the tile's grad_offset_mask segments (warp per pixel, coalesced); the last
+    // group run also zeroes the padding channels [3GK, S)
+    const bool last = tl.g0 + g.Gc == g.G;
+    for (int p = threadIdx.x >> 5; p < npix; p += blockDim.x >> 5) {
+      const int pho = tl.h0 + p / g.TW, pwo = tl.w0 + p % g.TW;
+      if (pho >= g.Ho || pwo >= g.Wo) continue;
+      T* dst = gom + ((long long)(tl.n * g.Ho + pho) * g.Wo + pwo) * g.S;
+      for (int e = lane; e < seg32; e += 32) dst[tl.g0 * 3 * K + e] = Elem<T>::from_f32(gtile[p * seg32 + e]);
+      if (last)
+        for (int e = g.G * 3 * K + lane; e < g.S; e += 32) dst[e] = Elem<T>::from_f32(0.f);
     }
   }
-  __syncthreads();
-  // coalesced write of the CTA's grad_offset_mask rows (padding channels stay 0)
-  T* gdst = gom + p_first * g.S;
-  for (int e = threadIdx.x; e < npix * g.S; e += blockDim.x) gdst[e] = Elem<T>::from_f32(gtile[e]);
+  cp_async_wait<0>();
 }
 
 // fp32 accumulator -> grad_input in T (half dtypes only); n16 = number of 16-B T chunks.

@@ -1,6 +1,7 @@
 // dcnv4_launch.h -- internal host-side launch description shared by the API and the
 // per-dtype instantiation units (not part of the C ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 
@@ -14,11 +15,14 @@ struct Launch {
   int lanes;        // nch / cpl lanes per (pixel, group)
   int ppc;          // output pixels per CTA
   int threads;      // CTA size (multiple of 32)
-  long long ctas;   // grid size
+  long long ctas;   // tiles (CTA work units); persistent grid = min(tiles, SMs x occupancy)
+  bool persistent;  // false: one CTA per tile (ablation)
   size_t smem;      // dynamic shared memory bytes
   bool k33;         // compile-time 3x3 path
   bool unit;        // offset_scale == 1 exact-split path
   cudaStream_t stream;
+  bool halo;        // forward: TMA halo kernel (else the global-gather kernel)
+  CUtensorMap xmap; // TMA descriptor of x for the halo kernel
 };
 
 #define DCNV4_DECLARE(SUFFIX)                                                              \
