@@ -229,8 +229,16 @@ TileChoice choose_tile(const dcnv4_params* p, int b, int nch, int cpl, int64_t H
 
 // TMA descriptor of x as a 4-D tensor {C, W, H, N} (innermost first) with a
 // {Gc*D, HW, HH, 1} box; out-of-image elements are zero-filled by the hardware.
+bool encode_nhwc_map(int dtype, const void* ptr, int64_t N, int64_t Hh, int64_t Ww, int64_t C,
+                     int box_c, int box_w, int box_h, CUtensorMap* map);
+
 bool encode_x_map(const dcnv4_params* p, int dtype, const void* x, int box_c, int box_w,
                   int box_h, CUtensorMap* map) {
+  return encode_nhwc_map(dtype, x, p->N, p->H, p->W, (int64_t)p->G * p->D, box_c, box_w, box_h, map);
+}
+
+bool encode_nhwc_map(int dtype, const void* ptr, int64_t N, int64_t Hh, int64_t Ww, int64_t Cc,
+                     int box_c, int box_w, int box_h, CUtensorMap* map) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -241,17 +249,26 @@ bool encode_x_map(const dcnv4_params* p, int dtype, const void* x, int box_c, in
   }();
   if (!encode) return false;
   const int b = elem_size(dtype);
-  const cuuint64_t C = (cuuint64_t)p->G * p->D;
-  const cuuint64_t dims[4] = {C, (cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->N};
-  const cuuint64_t strides[3] = {C * b, C * b * p->W, C * b * p->W * p->H};
+  const cuuint64_t C = (cuuint64_t)Cc;
+  const cuuint64_t dims[4] = {C, (cuuint64_t)Ww, (cuuint64_t)Hh, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {C * b, C * b * Ww, C * b * Ww * Hh};
   const cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUtensorMapDataType dt = dtype == DCNV4_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : dtype == DCNV4_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                       : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  const CUresult r = encode(map, dt, 4, const_cast<void*>(x), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  auto run = [&] {
+    return encode(map, dt, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  CUresult r = run();
+  if (r == CUDA_ERROR_INVALID_CONTEXT) {
+    // a thread that has not touched the runtime yet (e.g. torch's autograd worker) has
+    // no current context: bind the current device's primary context (same device)
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) r = run();
+  }
   return r == CUDA_SUCCESS;
 }
 
@@ -325,8 +342,102 @@ bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   return true;
 }
 
+// Backward on the paper's grid: TMA halo + binned (counting-sort) grad_input scatter
+// (bwd33_kernel).  Same tile as the forward; shared memory is single-buffered (two CTAs
+// per SM overlap each other's loads).  Needs x and gy pointers for the TMA maps.
+bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const void* x,
+                const void* gy, dcnv4::Launch* lc, dcnv4::Geo* g) {
+  const char* path = getenv("DCNV4_BWD_PATH");
+  if (path && path[0] == 'g') return false;
+  if (p->kernel_h != 3 || p->kernel_w != 3 || p->stride_h != 1 || p->stride_w != 1 ||
+      p->dilation_h != 1 || p->dilation_w != 1)
+    return false;
+  const int b = elem_size(dtype);
+  const int nch = lc->nch, cpl = lc->cpl, L = lc->lanes;
+  const int GC = nch >= 8 ? 1 : 8 / nch;
+  if (p->G % GC) return false;
+  const int DG = p->D;
+  const int PB = GC * DG * b;
+  const int per_row = 8 * GC * L;
+  int TH = 256 / per_row;
+  if (TH < 1) return false;
+  const char* th_env = getenv("DCNV4_BWD33_TH");
+  if (th_env && *th_env) TH = std::max(1, std::min(TH, atoi(th_env)));
+  if (TH > Ho) TH = (int)Ho;
+  const int K = 9;
+  const int S = p->om_stride ? p->om_stride : 3 * p->G * K;
+  const int segB_raw = GC * 3 * K * b;
+  int unit = 0;
+  for (int u : {8, 4})
+    if ((S * b) % u == 0 && segB_raw % u == 0) { unit = u; break; }
+  if (!unit) return false;
+  int seg_bytes = (segB_raw + 15) & ~15;
+  if ((seg_bytes / 16) % 2 == 0) seg_bytes += 16;
+  const int npix = TH * 8, HH = TH + 6, NT = HH * 14;
+  auto up = [](size_t v, size_t a) { return (v + a - 1) / a * a; };
+  size_t o = 0;
+  const int halo_box = HH * 14 * PB;
+  o = up((size_t)halo_box, 128);
+  const int o_gy = (int)o;
+  const int gy_box = npix * GC * DG * b;
+  o = up(o + gy_box, 128);
+  const int o_om = (int)o;
+  o = up(o + (size_t)npix * seg_bytes, 16);
+  const int o_gom = (int)o;
+  o = up(o + (size_t)npix * GC * 3 * K * 4, 16);
+  const int o_cnt = (int)o;
+  o = up(o + ((size_t)GC * NT + 1) * 4, 16);
+  const int o_slot = (int)o;
+  o = up(o + (size_t)npix * GC * 36 * 2, 16);
+  const int o_ent = (int)o;
+  o = up(o + (size_t)GC * npix * 36 * 8, 16);
+  const int o_wsum = (int)o;
+  o = up(o + 33 * 4, 16);
+  const int o_bar = (int)o;
+  const size_t smem = o + 16;
+  if (smem > 227 * 1024) return false;
+  const long long tiles_h = (Ho + TH - 1) / TH, tiles_w = (Wo + 7) / 8, gblocks = p->G / GC;
+  const long long tiles = (long long)p->N * tiles_h * tiles_w * gblocks;
+  if (tiles > 0x7fffffffLL) return false;
+  if (!x || !gy || reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(gy) % 16)
+    return false;
+  dcnv4::Launch l2 = *lc;
+  dcnv4::Geo g2 = *g;
+  if (!encode_x_map(p, dtype, x, GC * DG, 14, HH, &l2.xmap)) return false;
+  if (!encode_nhwc_map(dtype, gy, p->N, Ho, Wo, (int64_t)p->G * DG, GC * DG, 8, TH, &l2.gymap))
+    return false;
+  int shift;
+  conflict_factor(GC, L, cpl, nch, per_row * TH, &shift);
+  g2.TH = TH; g2.TW = 8; g2.Gc = GC;
+  g2.tiles_h = (int)tiles_h; g2.tiles_w = (int)tiles_w; g2.gblocks = (int)gblocks;
+  g2.tiles_total = (int)tiles;
+  g2.rot_shift = shift;
+  g2.seg = seg_bytes / b;
+  g2.HH = HH; g2.HW = 14;
+  g2.halo_box_bytes = halo_box;
+  g2.halo_bytes = (int)up((size_t)halo_box, 128);
+  g2.gy_box_bytes = gy_box;
+  g2.o_gy = o_gy; g2.o_om = o_om; g2.o_gom = o_gom; g2.o_cnt = o_cnt; g2.o_slot = o_slot;
+  g2.o_ent = o_ent; g2.o_wsum = o_wsum; g2.o_bar = o_bar;
+  g2.unit = unit;
+  g2.upp = segB_raw / unit;
+  g2.fd_gb = make_fastdiv((unsigned)gblocks);
+  g2.fd_tw = make_fastdiv((unsigned)tiles_w);
+  g2.fd_th = make_fastdiv((unsigned)tiles_h);
+  g2.fd_upp = make_fastdiv((unsigned)g2.upp);
+  l2.halo = true;
+  l2.ppc = npix;
+  l2.threads = per_row * TH;
+  l2.ctas = tiles;
+  l2.smem = smem;
+  *lc = l2;
+  *g = g2;
+  return true;
+}
+
 int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t Wo,
-                dcnv4::Launch* lc, dcnv4::Geo* g, const void* x = nullptr) {
+                dcnv4::Launch* lc, dcnv4::Geo* g, const void* x = nullptr,
+                const void* gy = nullptr) {
   const int b = elem_size(dtype);
   const int nch = p->D * b / 16;
   int cpl = default_cpl(nch, pass);
@@ -375,7 +486,10 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
   g->seg = seg_bytes / b;
   lc->halo = false;
   if (pass == 0) plan_fwd33(p, dtype, Ho, Wo, x, lc, g);
+  else plan_bwd33(p, dtype, Ho, Wo, x, gy, lc, g);
   g->tiles_total = (int)lc->ctas;
+  const char* dbg = getenv("DCNV4_DBG");
+  g->dbg = dbg ? atoi(dbg) : 0;
   const char* np = getenv("DCNV4_NONPERSISTENT");
   lc->persistent = !(np && *np == '1');
   return DCNV4_OK;
@@ -419,7 +533,8 @@ int dcnv4_launch_info(const dcnv4_params* p, dcnv4_dtype dtype, int pass, int32_
   if (rc) return rc;
   dcnv4::Launch lc;
   dcnv4::Geo g;
-  rc = make_launch(p, dtype, pass ? 1 : 0, Ho, Wo, &lc, &g, reinterpret_cast<const void*>(256));
+  rc = make_launch(p, dtype, pass ? 1 : 0, Ho, Wo, &lc, &g, reinterpret_cast<const void*>(256),
+                   reinterpret_cast<const void*>(256));
   if (rc) return rc;
   if (lanes) *lanes = lc.lanes;
   if (chunks_per_lane) *chunks_per_lane = lc.cpl;
@@ -495,7 +610,7 @@ int dcnv4_backward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input,
   }
   dcnv4::Launch lc;
   dcnv4::Geo g;
-  rc = make_launch(p, dtype, 1, Ho, Wo, &lc, &g);
+  rc = make_launch(p, dtype, 1, Ho, Wo, &lc, &g, input, grad_output);
   if (rc) return rc;
   lc.stream = static_cast<cudaStream_t>(stream);
   const size_t nelem = (size_t)p->N * p->H * p->W * p->G * p->D;

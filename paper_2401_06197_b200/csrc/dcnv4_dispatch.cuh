@@ -59,6 +59,20 @@ static cudaError_t bwd_variant(const Launch& lc, const Geo& g, const void* x, co
   const T* op = static_cast<const T*>(om);
   const T* gyp = static_cast<const T*>(gy);
   T* gomp = static_cast<T*>(gom);
+  if (lc.halo) {  // 3x3 / stride 1 / dilation 1: TMA halo + binned scatter
+    void (*hk)(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, Geo,
+               const T*, const T*, float*, T*);
+    if (lc.unit) hk = bwd33_kernel<T, NCH, CPL, true>;
+    else hk = bwd33_kernel<T, NCH, CPL, false>;
+    if (lc.smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)lc.smem);
+      if (e != cudaSuccess) return e;
+    }
+    hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(lc.xmap, lc.gymap, g, xp,
+                                                                            op, gx32, gomp);
+    return cudaGetLastError();
+  }
   void (*kern)(Geo, const T*, const T*, const T*, float*, T*);
   if (lc.k33 && lc.unit) kern = bwd_kernel<T, NCH, CPL, 3, 3, true>;
   else if (lc.k33) kern = bwd_kernel<T, NCH, CPL, 3, 3, false>;

@@ -58,6 +58,10 @@ struct Geo {
   int halo_box_bytes;              // bytes one TMA box delivers
   int upp, unit;                   // om staging: units per tile pixel, unit bytes (8 or 4)
   FastDiv fd_gb, fd_tw, fd_th, fd_upp;
+  // backward (bwd33) shared-memory carve-up (byte offsets) and TMA box of the gy tile
+  int gy_box_bytes;
+  int o_gy, o_om, o_gom, o_cnt, o_slot, o_ent, o_wsum, o_bar;
+  int dbg;  // profiling only (env DCNV4_DBG): bit0 skips the grad_input phases P2-P4
 };
 
 // ------------------------------------------------------------------ element types
@@ -824,6 +828,396 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x
     }
   }
   cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------ backward, 3x3 halo + binned scatter
+// One CTA tile (TH x 8 output pixels x GC groups) per iteration, persistent grid:
+//  P0  TMA: x halo ((TH+6) x 14 px) and the gy tile; cp.async: offset_mask rows
+//  P1  per (pixel, group) lane group, the 9 samples from the shared-memory halo:
+//        S_q = <gy, x_q> (4 dot products per sample), grad_m / grad_offset partials
+//        reduced over the L lanes -> grad_om tile; every in-image corner contribution
+//        a = m*w_q (the bilinear scatter weight) is counted into its halo target bin
+//        (native shared atomic ATOMS.ADD; fp32 shared atomics would be CAS loops)
+//  P2  exclusive scan of the bin counts
+//  P3  contributions written (a, source pixel) into their bins (counting sort)
+//  P4  per (halo pixel, group, 16-B chunk): gx = sum_bin a * gy[source] from shared
+//      memory, then ONE 16-B vector reduction into the fp32 grad_input accumulator --
+//      ~3x the tile's pixels instead of 36 per (pixel, group) (the v3 kernel was bound
+//      by L2 reduction throughput, profiles/r01_v1_*).
+// Samples leaving the halo (|offset| >= 2 px) take a bounds-checked global path with
+// direct vector reductions.
+// v[q] for a runtime q in [0, 4) without dynamic register-array indexing (no local memory)
+template <typename V>
+__device__ __forceinline__ V pick4(const V* v, int q) {
+  const V lo = (q & 1) ? v[1] : v[0];
+  const V hi = (q & 1) ? v[3] : v[2];
+  return (q & 2) ? hi : lo;
+}
+
+__device__ __forceinline__ int block_exclusive_scan(int* data, int n, int* warp_sums) {
+  // in-place exclusive prefix sum of data[0..n) by the whole CTA; returns the total
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n + nt - 1) / nt;
+  const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
+  int local = 0;
+  for (int i = b0; i < b1; ++i) local += data[i];
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = nt >> 5;
+    int ws = lane < nw ? warp_sums[lane] : 0;
+    int wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    if (lane < nw) warp_sums[lane] = wi - ws;  // exclusive per warp
+    if (lane == nw - 1) warp_sums[32] = wi;    // total
+  }
+  __syncthreads();
+  int run = warp_sums[warp] + incl - local;
+  for (int i = b0; i < b1; ++i) {
+    const int v = data[i];
+    data[i] = run;
+    run += v;
+  }
+  const int total = warp_sums[32];
+  __syncthreads();
+  return total;
+}
+
+template <typename T, int NCH, int CPL, bool UNIT>
+__global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUtensorMap xmap,
+                                                    const __grid_constant__ CUtensorMap gymap, Geo g,
+                                                    const T* __restrict__ x,
+                                                    const T* __restrict__ om,
+                                                    float* __restrict__ gx32,
+                                                    T* __restrict__ gom) {
+  constexpr int L = NCH / CPL;
+  constexpr int E = Elem<T>::E;
+  constexpr int GC = NCH >= 8 ? 1 : 8 / NCH;
+  constexpr int DG = NCH * E;  // channels per group (compile-time)
+  constexpr int PB = GC * DG * (int)sizeof(T);
+  constexpr int TW = 8, HWC = 14, ROWB = HWC * PB;
+  constexpr int K = 9;
+  constexpr int QPL = L >= 4 ? 1 : 4 / L;  // corners whose scatter this lane owns
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int TH = g.TH, HH = TH + 6, NT = HH * HWC;
+  const int npix = TH * TW;
+  const T* gyt = reinterpret_cast<const T*>(smem + g.o_gy);
+  T* const omt = reinterpret_cast<T*>(smem + g.o_om);
+  float* const gomt = reinterpret_cast<float*>(smem + g.o_gom);
+  int* const cnt = reinterpret_cast<int*>(smem + g.o_cnt);
+  unsigned short* const slots = reinterpret_cast<unsigned short*>(smem + g.o_slot);
+  uint2* const ent = reinterpret_cast<uint2*>(smem + g.o_ent);
+  int* const wsum = reinterpret_cast<int*>(smem + g.o_wsum);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + g.o_bar);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int lg = tid % L;
+  const int gl = (tid / L) % GC;
+  const int px = (tid / (L * GC)) % TW;
+  const int py = tid / (L * GC * TW);
+  const bool slot_ok = py < TH;
+  const int item = (py * TW + px) * GC + gl;  // (pixel, group) index inside the tile
+  const unsigned gmask = (L >= 32 ? 0xffffffffu : ((1u << L) - 1u)) << (lane & ~(L - 1));
+  const int rot = g.rot_shift < 0 ? 0 : (((tid & 31) / L) >> g.rot_shift) & (CPL - 1);
+  int co[CPL];
+  uint32_t hb[CPL];
+#pragma unroll
+  for (int h = 0; h < CPL; ++h) {
+    co[h] = (((h + rot) & (CPL - 1)) * L + lg) * E;
+    hb[h] = smem_u32(smem) + (uint32_t)(gl * DG * (int)sizeof(T) + co[h] * (int)sizeof(T));
+  }
+  const int H = g.H, W = g.W, C = g.C;
+  const float s = g.s;
+  const unsigned segB = (unsigned)g.seg * sizeof(T);
+
+  for (int t = blockIdx.x, it = 0; t < g.tiles_total; t += gridDim.x, ++it) {
+    int n, h0, w0, g0;
+    {
+      const unsigned q1 = fdiv((unsigned)t, g.fd_gb);
+      g0 = (t - (int)q1 * g.gblocks) * GC;
+      const unsigned q2 = fdiv(q1, g.fd_tw);
+      w0 = ((int)q1 - (int)q2 * g.tiles_w) * TW;
+      const unsigned q3 = fdiv(q2, g.fd_th);
+      h0 = ((int)q2 - (int)q3 * g.tiles_h) * TH;
+      n = (int)q3;
+    }
+    const int hy0 = h0 - g.ph - 2, hx0 = w0 - g.pw - 2;  // halo origin in input pixels
+    // ---- P0: loads
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, (uint32_t)(g.halo_box_bytes + g.gy_box_bytes));
+      tma_load_4d(smem, &xmap, g0 * DG, hx0, hy0, n, bar);
+      tma_load_4d(smem + g.o_gy, &gymap, g0 * DG, w0, h0, n, bar);
+    }
+    {
+      const char* src0 = reinterpret_cast<const char*>(
+          om + ((long long)(n * g.Ho + h0) * g.Wo + w0) * g.S + g0 * 3 * K);
+      unsigned char* dst0 = reinterpret_cast<unsigned char*>(omt);
+      const unsigned rowS = (unsigned)g.Wo * g.S * sizeof(T), pixS = (unsigned)g.S * sizeof(T);
+      for (int f = tid; f < npix * g.upp; f += blockDim.x) {
+        const int pix = (int)fdiv((unsigned)f, g.fd_upp);
+        const int u = f - pix * g.upp;
+        const int ppy = pix / TW, ppx = pix % TW;
+        if (h0 + ppy >= g.Ho || w0 + ppx >= g.Wo) continue;
+        const char* src = src0 + (ppy * rowS + ppx * pixS + (unsigned)(u * g.unit));
+        unsigned char* dst = dst0 + pix * segB + u * g.unit;
+        if (g.unit == 8) cp_async<8>(dst, src);
+        else cp_async<4>(dst, src);
+      }
+      cp_async_commit();
+    }
+    for (int i = tid; i < GC * NT; i += blockDim.x) cnt[i] = 0;
+    cp_async_wait<0>();
+    mbar_wait(bar, (uint32_t)(it & 1));
+    __syncthreads();
+
+    const int ho = h0 + py, wo = w0 + px;
+    const bool active = slot_ok && ho < g.Ho && wo < g.Wo;  // uniform over the L-lane group
+    const T* row = omt + (py * TW + px) * g.seg + gl * 3 * K;
+    float m[K];
+    float gyv[CPL * E];
+    unsigned outside = 0;
+    // ---- P1: grad_om and bin counts
+    if (active) {
+      load_m<T, K>(row, g.softmax, m);
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        uint4 u = *reinterpret_cast<const uint4*>(gyt + (py * TW + px) * GC * DG + gl * DG + co[h]);
+        Elem<T>::unpack(u, gyv + h * E);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int i = k / 3, j = k % 3;
+        const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
+        float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
+        float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
+        const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
+        ty = fin ? ty : 0.f;
+        tx = fin ? tx : 0.f;
+        const float fly = floorf(ty), flx = floorf(tx);
+        const float fy = ty - fly, fx = tx - flx;
+        const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
+        const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
+        const bool in = fin && (unsigned)yl <= (unsigned)(HH - 2) && (unsigned)xl <= (unsigned)(HWC - 2);
+        outside |= (fin && !in) ? (1u << k) : 0u;
+        const int ylc = in ? yl : 0, xlc = in ? xl : 0;
+        const uint32_t off = (uint32_t)(ylc * ROWB + xlc * PB);
+        float S[4];
+        float2 S2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) {
+          const uint32_t a0 = hb[h] + off;
+          uint4 u[4] = {lds16(a0), lds16(a0 + PB), lds16(a0 + ROWB), lds16(a0 + ROWB + PB)};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float v[E];
+            Elem<T>::unpack(u[q], v);
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {  // FFMA2 over channel pairs
+              const float2 r = __ffma2_rn(make_float2(gyv[h * E + e], gyv[h * E + e + 1]),
+                                          make_float2(v[e], v[e + 1]), S2[q]);
+              S2[q] = r;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S[q] = S2[q].x + S2[q].y;
+        // corner validity (inside the image); halo pixels outside the image hold zeros
+        const int yy = hy0 + ylc, xx = hx0 + xlc;
+        const bool vy0 = (unsigned)yy < (unsigned)H, vy1 = (unsigned)(yy + 1) < (unsigned)H;
+        const bool vx0 = (unsigned)xx < (unsigned)W, vx1 = (unsigned)(xx + 1) < (unsigned)W;
+        const bool ok[4] = {in && vy0 && vx0, in && vy0 && vx1, in && vy1 && vx0, in && vy1 && vx1};
+        const float hy = 1.f - fy, hx = 1.f - fx;
+        const float w[4] = {hy * hx, hy * fx, fy * hx, fy * fx};
+        float sgm = w[0] * S[0] + w[1] * S[1] + w[2] * S[2] + w[3] * S[3];
+        float sgy = hx * (S[2] - S[0]) + fx * (S[3] - S[1]);
+        float sgx = hy * (S[1] - S[0]) + fy * (S[3] - S[2]);
+#pragma unroll
+        for (int o = 1; o < L; o <<= 1) {
+          sgm += __shfl_xor_sync(gmask, sgm, o);
+          sgy += __shfl_xor_sync(gmask, sgy, o);
+          sgx += __shfl_xor_sync(gmask, sgx, o);
+        }
+        if (lg == 0) {
+          float* grow = gomt + item * 3 * K;
+          grow[2 * k] = in ? s * m[k] * sgx : 0.f;
+          grow[2 * k + 1] = in ? s * m[k] * sgy : 0.f;
+          grow[2 * K + k] = in ? sgm : 0.f;
+        }
+        // count this lane's scatter contributions into their halo bins
+#pragma unroll
+        for (int r = 0; r < QPL; ++r) {
+          const int q = (lg % 4) + r * L;
+          if (lg < 4 && q < 4 && pick4(ok, q) && m[k] * pick4(w, q) != 0.f) {
+            const int tt = (ylc + (q >> 1)) * HWC + xlc + (q & 1);
+            slots[item * 36 + k * 4 + q] = (unsigned short)atomicAdd(&cnt[gl * NT + tt], 1);
+          }
+        }
+      }
+      if (outside) {  // rare: samples beyond the halo -- global gathers and reductions
+        const T* ximg = x + (long long)n * H * W * C;
+        float* gximg = gx32 + (long long)n * H * W * C;
+        const unsigned gbase = (g0 + gl) * DG;
+        float smx = 0.f, sinv = 1.f;
+        if (g.softmax) softmax_stats<T>(row, K, smx, sinv);
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+          if (!((outside >> k) & 1u)) continue;
+          const int i = k / 3, j = k % 3;
+          float mk = Elem<T>::f(row[2 * K + k]);
+          if (g.softmax) mk = __expf(mk - smx) * sinv;
+          Samp c;
+          sample<UNIT>(H, W, C, s, ho - g.ph + 1, wo - g.pw + 1, j - 1, i - 1,
+                       Elem<T>::f(row[2 * k]), Elem<T>::f(row[2 * k + 1]), gbase, c);
+          float S[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int h = 0; h < CPL; ++h) {
+              float v[E];
+              Elem<T>::unpack(ldg16_idx<sizeof(T)>(ximg + co[h], c.o[q]), v);
+#pragma unroll
+              for (int e = 0; e < E; ++e) S[q] = fmaf(gyv[h * E + e], v[e], S[q]);
+            }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (!c.ok[q]) S[q] = 0.f;
+            const float a = mk * c.w[q];
+            if (a != 0.f)
+#pragma unroll
+              for (int h = 0; h < CPL; ++h)
+#pragma unroll
+                for (int e = 0; e < E; e += 4)
+                  red_add_v4_idx(gximg + co[h] + e, c.o[q], a * gyv[h * E + e], a * gyv[h * E + e + 1],
+                                 a * gyv[h * E + e + 2], a * gyv[h * E + e + 3]);
+          }
+          const float hy = 1.f - c.fy, hx = 1.f - c.fx;
+          float sgm = c.w[0] * S[0] + c.w[1] * S[1] + c.w[2] * S[2] + c.w[3] * S[3];
+          float sgy = hx * (S[2] - S[0]) + c.fx * (S[3] - S[1]);
+          float sgx = hy * (S[1] - S[0]) + c.fy * (S[3] - S[2]);
+#pragma unroll
+          for (int o = 1; o < L; o <<= 1) {
+            sgm += __shfl_xor_sync(gmask, sgm, o);
+            sgy += __shfl_xor_sync(gmask, sgy, o);
+            sgx += __shfl_xor_sync(gmask, sgx, o);
+          }
+          if (lg == 0) {
+            float* grow = gomt + item * 3 * K;
+            grow[2 * k] = s * mk * sgx;
+            grow[2 * k + 1] = s * mk * sgy;
+            grow[2 * K + k] = sgm;
+          }
+        }
+      }
+      if (g.softmax && lg == 0) {  // dL/dz_k = p_k (gm_k - sum_j p_j gm_j)
+        float* grow = gomt + item * 3 * K;
+        float dot = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) dot += m[k] * grow[2 * K + k];
+#pragma unroll
+        for (int k = 0; k < K; ++k) grow[2 * K + k] = m[k] * (grow[2 * K + k] - dot);
+      }
+    }
+    __syncthreads();
+    // ---- P2: bin offsets (one in-place exclusive scan over all groups' bins;
+    // bin i holds entries [offs[i], offs[i+1]))
+    int* const offs = cnt;
+    if (g.dbg & 1) { __syncthreads(); continue; }
+    {
+      const int total = block_exclusive_scan(offs, GC * NT, wsum);
+      if (tid == 0) offs[GC * NT] = total;
+      __syncthreads();
+    }
+    // ---- P3: fill the bins; write the grad_om tile
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if ((outside >> k) & 1u) continue;
+        const int i = k / 3, j = k % 3;
+        const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
+        float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
+        float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
+        const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
+        if (!fin) continue;
+        const float fly = floorf(ty), flx = floorf(tx);
+        const float fy = ty - fly, fx = tx - flx;
+        const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
+        const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
+        const int yy = hy0 + yl, xx = hx0 + xl;
+        const bool vy0 = (unsigned)yy < (unsigned)H, vy1 = (unsigned)(yy + 1) < (unsigned)H;
+        const bool vx0 = (unsigned)xx < (unsigned)W, vx1 = (unsigned)(xx + 1) < (unsigned)W;
+        const bool ok[4] = {vy0 && vx0, vy0 && vx1, vy1 && vx0, vy1 && vx1};
+        const float hy = 1.f - fy, hx = 1.f - fx;
+        const float w[4] = {hy * hx, hy * fx, fy * hx, fy * fx};
+#pragma unroll
+        for (int r = 0; r < QPL; ++r) {
+          const int q = (lg % 4) + r * L;
+          const float a = m[k] * pick4(w, q);
+          if (lg < 4 && q < 4 && pick4(ok, q) && a != 0.f) {
+            const int tt = (yl + (q >> 1)) * HWC + xl + (q & 1);
+            const int e = offs[gl * NT + tt] + slots[item * 36 + k * 4 + q];
+            ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
+          }
+        }
+      }
+    }
+    {
+      const bool last = g0 + GC == g.G;
+      for (int p = tid >> 5; p < npix; p += blockDim.x >> 5) {
+        const int pho = h0 + p / TW, pwo = w0 + p % TW;
+        if (pho >= g.Ho || pwo >= g.Wo) continue;
+        T* dst = gom + ((long long)(n * g.Ho + pho) * g.Wo + pwo) * g.S;
+        for (int e = lane; e < GC * 3 * K; e += 32)
+          dst[g0 * 3 * K + e] = Elem<T>::from_f32(gomt[p * GC * 3 * K + e]);
+        if (last)
+          for (int e = g.G * 3 * K + lane; e < g.S; e += 32) dst[e] = Elem<T>::from_f32(0.f);
+      }
+    }
+    __syncthreads();
+    // ---- P4: pull per (halo pixel, group, chunk) and one vector reduction each
+    {
+      float* gximg = gx32 + (long long)n * H * W * C;
+      for (int f = tid; f < NT * GC * NCH; f += blockDim.x) {
+        const int c = f % NCH;
+        const int gg = (f / NCH) % GC;
+        const int tt = f / (NCH * GC);
+        const int b0 = offs[gg * NT + tt];
+        const int ne = offs[gg * NT + tt + 1] - b0;
+        if (ne == 0) continue;
+        const uint2* b = ent + b0;
+        float acc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = 0.f;
+        for (int q = 0; q < ne; ++q) {
+          const uint2 en = b[q];
+          const uint4 u = *reinterpret_cast<const uint4*>(gyt + en.y * (GC * DG) + gg * DG + c * E);
+          float v[E];
+          Elem<T>::unpack(u, v);
+          axpy2<E>(acc, __uint_as_float(en.x), v);
+        }
+        const int yy = hy0 + tt / HWC, xx = hx0 + tt % HWC;
+        float* dst = gximg + ((unsigned)(yy * W + xx) * C + (g0 + gg) * DG + c * E);
+#pragma unroll
+        for (int e = 0; e < E; e += 4) red_add_v4(dst + e, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+      }
+    }
+    __syncthreads();  // shared memory is reused by the next tile
+  }
 }
 
 // fp32 accumulator -> grad_input in T (half dtypes only); n16 = number of 16-B T chunks.

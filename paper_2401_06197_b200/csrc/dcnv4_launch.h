@@ -22,7 +22,8 @@ struct Launch {
   bool unit;        // offset_scale == 1 exact-split path
   cudaStream_t stream;
   bool halo;        // forward: TMA halo kernel (else the global-gather kernel)
-  CUtensorMap xmap; // TMA descriptor of x for the halo kernel
+  CUtensorMap xmap; // TMA descriptor of x for the halo kernels
+  CUtensorMap gymap;  // TMA descriptor of grad_output (backward halo kernel)
 };
 
 #define DCNV4_DECLARE(SUFFIX)                                                              \
