@@ -126,17 +126,13 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- helpers
 def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    from paper_2401_06197_b200.sharding import dist_env
+    return dist_env()
 
 
 def _shard(batch, ws, rank, shard):
-    if not shard:
-        return list(range(batch))
-    per = batch // ws
-    return list(range(rank * per, (rank + 1) * per))
+    from paper_2401_06197_b200.sharding import shard_images
+    return shard_images(batch, ws, rank) if shard else list(range(batch))
 
 
 def _alg_bytes(x, om, backward):
