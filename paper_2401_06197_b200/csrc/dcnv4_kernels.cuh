@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           const int q = (lg % 4) + r * L;
           if (lg < 4 && q < 4 && pick4(ok, q) && m[k] * pick4(w, q) != 0.f) {
             const int tt = (ylc + (q >> 1)) * HWC + xlc + (q & 1);
-            slots[item * 36 + k * 4 + q] = (unsigned short)atomicAdd(&cnt[gl * NT + tt], 1);
+            slots[(k * 4 + q) * (npix * GC) + item] = (unsigned short)atomicAdd(&cnt[gl * NT + tt], 1);
           }
         }
       }
@@ -1170,7 +1170,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           const float a = m[k] * pick4(w, q);
           if (lg < 4 && q < 4 && pick4(ok, q) && a != 0.f) {
             const int tt = (yl + (q >> 1)) * HWC + xl + (q & 1);
-            const int e = offs[gl * NT + tt] + slots[item * 36 + k * 4 + q];
+            const int e = offs[gl * NT + tt] + slots[(k * 4 + q) * (npix * GC) + item];
             ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
           }
         }
