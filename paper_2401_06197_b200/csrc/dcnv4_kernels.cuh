@@ -474,6 +474,68 @@ __device__ __forceinline__ void axpy2(float* acc, float a, const float* v) {
   }
 }
 
+// acc[0..E) += a * chunk, the chunk being one 16-byte vector of T:
+//   fp32      -> 2 FFMA2 (packed fp32 pairs)
+//   fp16/bf16 -> 8 FHFMA (sm_100 mixed-precision fma.rn.f32.{f16,bf16}: half x half + f32,
+//                reading both halves of each register with no unpack); the weight a is
+//                rounded to T once (relative error <= 2^-11 / 2^-8 per term, within the
+//                1e-2 half-precision tolerance; R10)
+template <typename T>
+__device__ __forceinline__ void fma_chunk(float* acc, float a, const uint4& u);
+template <>
+__device__ __forceinline__ void fma_chunk<float>(float* acc, float a, const uint4& u) {
+  float v[4];
+  Elem<float>::unpack(u, v);
+  axpy2<4>(acc, a, v);
+}
+template <>
+__device__ __forceinline__ void fma_chunk<__half>(float* acc, float a, const uint4& u) {
+  const unsigned short ah = __half_as_ushort(__float2half_rn(a));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+        "fma.rn.f32.f16 %0, %3, l, %0;\n\tfma.rn.f32.f16 %1, %3, h, %1;\n\t}"
+        : "+f"(acc[2 * i]), "+f"(acc[2 * i + 1])
+        : "r"(w[i]), "h"(ah));
+}
+template <>
+__device__ __forceinline__ void fma_chunk<__nv_bfloat16>(float* acc, float a, const uint4& u) {
+  const unsigned short ah = __bfloat16_as_ushort(__float2bfloat16_rn(a));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, %3, l, %0;\n\tfma.rn.f32.bf16 %1, %3, h, %1;\n\t}"
+        : "+f"(acc[2 * i]), "+f"(acc[2 * i + 1])
+        : "r"(w[i]), "h"(ah));
+}
+
+// S += <g, x> over one 16-byte chunk (two partial sums).  For fp16/bf16 both operands stay
+// packed and FHFMA multiplies half x half exactly into the fp32 accumulator.
+template <typename T>
+__device__ __forceinline__ void dot_chunk(float2& S, const uint4& g, const uint4& x);
+template <>
+__device__ __forceinline__ void dot_chunk<float>(float2& S, const uint4& g, const uint4& x) {
+  S = __ffma2_rn(make_float2(__uint_as_float(g.x), __uint_as_float(g.y)),
+                 make_float2(__uint_as_float(x.x), __uint_as_float(x.y)), S);
+  S = __ffma2_rn(make_float2(__uint_as_float(g.z), __uint_as_float(g.w)),
+                 make_float2(__uint_as_float(x.z), __uint_as_float(x.w)), S);
+}
+#define DCNV4_DOT_HALF(TY, PTXT)                                                                  \
+  template <>                                                                                     \
+  __device__ __forceinline__ void dot_chunk<TY>(float2& S, const uint4& g, const uint4& x) {      \
+    const uint32_t gw[4] = {g.x, g.y, g.z, g.w}, xw[4] = {x.x, x.y, x.z, x.w};                    \
+    _Pragma("unroll") for (int i = 0; i < 4; ++i)                                                 \
+      asm("{\n\t.reg .b16 gl, gh, xl, xh;\n\tmov.b32 {gl, gh}, %2;\n\tmov.b32 {xl, xh}, %3;\n\t" \
+          "fma.rn.f32." PTXT " %0, gl, xl, %0;\n\tfma.rn.f32." PTXT " %1, gh, xh, %1;\n\t}"        \
+          : "+f"(S.x), "+f"(S.y)                                                                  \
+          : "r"(gw[i]), "r"(xw[i]));                                                              \
+  }
+DCNV4_DOT_HALF(__half, "f16")
+DCNV4_DOT_HALF(__nv_bfloat16, "bf16")
+#undef DCNV4_DOT_HALF
+
 template <typename T, int NCH, int CPL, bool UNIT>
 __global__ void __launch_bounds__(256) fwd33_kernel(const __grid_constant__ CUtensorMap xmap, Geo g,
                                                     const T* __restrict__ x,
@@ -615,11 +677,7 @@ __global__ void __launch_bounds__(256) fwd33_kernel(const __grid_constant__ CUte
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int h = 0; h < CPL; ++h) {
-            float v[E];
-            Elem<T>::unpack(F.u[q][h], v);
-            axpy2<E>(acc + h * E, F.a[q], v);
-          }
+          for (int h = 0; h < CPL; ++h) fma_chunk<T>(acc + h * E, F.a[q], F.u[q][h]);
       };
       // software pipeline: the gathers of point k+1 are issued before the FMAs of k
       Fetched F0, F1;
@@ -990,6 +1048,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
     const T* row = omt + (py * TW + px) * g.seg + gl * 3 * K;
     float m[K];
     float gyv[CPL * E];
+    uint4 gyu[CPL];  // the lane's gy chunks, packed (dot products)
     unsigned outside = 0;
     // ---- P1: grad_om and bin counts
     if (active) {
@@ -997,6 +1056,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
 #pragma unroll
       for (int h = 0; h < CPL; ++h) {
         uint4 u = *reinterpret_cast<const uint4*>(gyt + (py * TW + px) * GC * DG + gl * DG + co[h]);
+        gyu[h] = u;
         Elem<T>::unpack(u, gyv + h * E);
       }
 #pragma unroll
@@ -1024,16 +1084,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           const uint32_t a0 = hb[h] + off;
           uint4 u[4] = {lds16(a0), lds16(a0 + PB), lds16(a0 + ROWB), lds16(a0 + ROWB + PB)};
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float v[E];
-            Elem<T>::unpack(u[q], v);
-#pragma unroll
-            for (int e = 0; e < E; e += 2) {  // FFMA2 over channel pairs
-              const float2 r = __ffma2_rn(make_float2(gyv[h * E + e], gyv[h * E + e + 1]),
-                                          make_float2(v[e], v[e + 1]), S2[q]);
-              S2[q] = r;
-            }
-          }
+          for (int q = 0; q < 4; ++q) dot_chunk<T>(S2[q], gyu[h], u[q]);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) S[q] = S2[q].x + S2[q].y;
@@ -1206,9 +1257,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
         for (int q = 0; q < ne; ++q) {
           const uint2 en = b[q];
           const uint4 u = *reinterpret_cast<const uint4*>(gyt + en.y * (GC * DG) + gg * DG + c * E);
-          float v[E];
-          Elem<T>::unpack(u, v);
-          axpy2<E>(acc, __uint_as_float(en.x), v);
+          fma_chunk<T>(acc, __uint_as_float(en.x), u);
         }
         const int yy = hy0 + tt / HWC, xx = hx0 + tt % HWC;
         float* dst = gximg + ((unsigned)(yy * W + xx) * C + (g0 + gg) * DG + c * E);
