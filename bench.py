@@ -148,7 +148,7 @@ def _traffic(workload, kind):
     try:
         with open(path) as f:
             t = json.load(f)
-        return t[workload][kind]
+        return int(t[workload][kind])
     except Exception:
         return None
 

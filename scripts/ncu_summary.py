@@ -62,6 +62,8 @@ def launches(path):
         name = r[hdr.index("Kernel Name")]
         unit = r[hdr.index("Metric Unit")]
         v = float(r[hdr.index("Metric Value")].replace(",", ""))
+        if v != v:  # nan: a graph-capture placeholder launch (grid 0x0x0)
+            continue
         v = v / 1000.0 if unit in ("nsecond", "ns") else (v * 1000.0 if unit in ("msecond", "ms") else v)
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
