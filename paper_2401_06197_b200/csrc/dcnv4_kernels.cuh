@@ -1240,29 +1240,43 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       }
     }
     __syncthreads();
-    // ---- P4: pull per (halo pixel, group, chunk) and one vector reduction each
+    // ---- P4: pull per (halo pixel, group, PC chunks) and one vector reduction per chunk;
+    // PC = 2 chunks per lane amortise the entry loads; the chunk order alternates with
+    // the halo pixel so an 8-lane phase still touches 8 distinct bank quads
     {
+      constexpr int PC = NCH >= 2 ? 2 : 1;
+      constexpr int NCL = NCH / PC;  // lanes per (halo pixel, group)
       float* gximg = gx32 + (long long)n * H * W * C;
-      for (int f = tid; f < NT * GC * NCH; f += blockDim.x) {
-        const int c = f % NCH;
-        const int gg = (f / NCH) % GC;
-        const int tt = f / (NCH * GC);
+      for (int f = tid; f < NT * GC * NCL; f += blockDim.x) {
+        const int cl = f % NCL;
+        const int gg = (f / NCL) % GC;
+        const int tt = f / (NCL * GC);
         const int b0 = offs[gg * NT + tt];
         const int ne = offs[gg * NT + tt + 1] - b0;
         if (ne == 0) continue;
         const uint2* b = ent + b0;
-        float acc[E];
+        int cc[PC];
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc[e] = 0.f;
+        for (int h = 0; h < PC; ++h) cc[h] = (cl * PC + ((h + tt) & (PC - 1))) * E;
+        float acc[PC * E];
+#pragma unroll
+        for (int e = 0; e < PC * E; ++e) acc[e] = 0.f;
+        const T* gyg = gyt + gg * DG;
         for (int q = 0; q < ne; ++q) {
           const uint2 en = b[q];
-          const uint4 u = *reinterpret_cast<const uint4*>(gyt + en.y * (GC * DG) + gg * DG + c * E);
-          fma_chunk<T>(acc, __uint_as_float(en.x), u);
+          const T* src = gyg + en.y * (GC * DG);
+#pragma unroll
+          for (int h = 0; h < PC; ++h)
+            fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src + cc[h]));
         }
         const int yy = hy0 + tt / HWC, xx = hx0 + tt % HWC;
-        float* dst = gximg + ((unsigned)(yy * W + xx) * C + (g0 + gg) * DG + c * E);
+        float* dst = gximg + ((unsigned)(yy * W + xx) * C + (g0 + gg) * DG);
 #pragma unroll
-        for (int e = 0; e < E; e += 4) red_add_v4(dst + e, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+        for (int h = 0; h < PC; ++h)
+#pragma unroll
+          for (int e = 0; e < E; e += 4)
+            red_add_v4(dst + cc[h] + e, acc[h * E + e], acc[h * E + e + 1], acc[h * E + e + 2],
+                       acc[h * E + e + 3]);
       }
     }
     __syncthreads();  // shared memory is reused by the next tile
