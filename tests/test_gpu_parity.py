@@ -125,6 +125,14 @@ CASES = [
     ("softmax_v3", _geom(2, 9, 10, 2, 16, softmax=True), "u2"),
     ("softmax_k5", _geom(1, 8, 9, 2, 16, k=(5, 5), p=(2, 2), softmax=True), "u2"),
     ("single_pixel", _geom(1, 1, 1, 2, 16), "u2"),
+    # TMA-halo kernels (3x3/s1/d1) with group counts that suit the half-precision tiles
+    ("halo_G4_u8", _geom(2, 16, 16, 4, 16), "u8"),
+    ("halo_G8_ragged", _geom(2, 11, 13, 8, 16), "u2"),
+    ("halo_G4_scale0.5", _geom(2, 12, 10, 4, 16, scale=0.5), "u2"),
+    ("halo_G4_pad0", _geom(2, 12, 17, 4, 16, p=(0, 0)), "u2"),
+    ("halo_G4_pad2", _geom(1, 9, 10, 4, 16, p=(2, 2)), "u2"),
+    ("halo_G4_softmax", _geom(2, 10, 9, 4, 16, softmax=True), "u8"),
+    ("halo_G4_zero", _geom(2, 10, 9, 4, 16), "zero"),
 ]
 
 
