@@ -232,6 +232,8 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--global-batch", type=int, default=0)
     ap.add_argument("--offsets", default="u2", choices=["u2", "zero", "u8", "smooth"])
+    ap.add_argument("--softmax", action="store_true",
+                    help="DCNv3 mode (softmax over K, NEXT-1) instead of DCNv4")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -275,11 +277,14 @@ def main():
             st["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         stages.append(st)
 
+    sm = bool(args.softmax)
+
     def calls(st):
-        out = [("fwd", lambda st=st: pkg.forward(st["x"], st["om"], group=st["G"], out=st["y"]))]
+        out = [("fwd", lambda st=st: pkg.forward(st["x"], st["om"], group=st["G"], softmax=sm,
+                                                 out=st["y"]))]
         if cfg["backward"]:
             out.append(("bwd", lambda st=st: pkg.backward(
-                st["x"], st["om"], st["gy"], group=st["G"], grad_input=st["gx"],
+                st["x"], st["om"], st["gy"], group=st["G"], softmax=sm, grad_input=st["gx"],
                 grad_offset_mask=st["gom"], workspace=st["ws"])))
         return out
 
@@ -294,9 +299,9 @@ def main():
     verify = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.no_verify:
         # cpu_baseline leg (the only place bench.py runs oracle/): first image vs fp64 oracle
-        verify = _verify(cfg, stages, images)
+        verify = _verify(cfg, stages, images, softmax=sm)
     elif ws > 1 and not args.no_verify:
-        verify = _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist)
+        verify = _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist, sm)
 
     # ---- warm-up (eager), then capture K steps with event nodes between calls
     with torch.cuda.stream(stream):
@@ -376,8 +381,9 @@ def main():
     launches_dom = len(stages)
     achieved = kind_bytes[dom] / (kind_ms[dom] * 1e-3) / 1e9
     share = kind_ms[dom] / sum(kind_ms.values())
-    roofline = {"bound": "hbm", "kernel": f"dcnv4 {dom} ({'zero-fill + ' if dom == 'bwd' else ''}"
-                                          f"{dom}_kernel), {launches_dom} launches per step",
+    # every bench workload is 3x3 / stride 1 / dilation 1, i.e. the TMA-halo kernels
+    kname = "memset + bwd33_kernel" if dom == "bwd" else "fwd33_kernel"
+    roofline = {"bound": "hbm", "kernel": f"dcnv4 {dom} ({kname}), {launches_dom} launches per step",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "traffic": _traffic(cfg["name"], dom), "share_of_step": round(share, 4),
@@ -401,6 +407,7 @@ def main():
         "config": {"workload": cfg["name"], "desc": cfg["desc"], "global_batch": cfg["batch"],
                    "per_gpu_batch": n_img, "stages": [f"{h}x{w}x{g * D} G{g}" for h, w, g in cfg["stages"]],
                    "D": D, "kernel": "3x3 s1 p1 d1", "offset_scale": 1.0, "offsets": args.offsets,
+                   "operator": "DCNv3 (softmax over K)" if sm else "DCNv4",
                    "parallelism": f"batch-sharded dp{ws}" if cfg["shard"] else f"replicas x{ws}",
                    "l2": f"inputs larger than L2: per-rank working set "
                          f"{sum(_alg_bytes(s['x'], s['om'], cfg['backward']) for s in stages) / 1e9:.2f} GB "
@@ -430,14 +437,14 @@ def main():
     return 0
 
 
-def _verify(cfg, stages, images):
+def _verify(cfg, stages, images, softmax=False):
     """Oracle check of the shard's first image on every stage (outside the timed region)."""
     import numpy as np
     import oracle
     out = {}
     tol = 1e-5 if cfg["dtype"] == "f32" else 1e-2
     for st in stages:
-        g = oracle.Geometry(N=1, H=st["H"], W=st["W"], G=st["G"], D=D)
+        g = oracle.Geometry(N=1, H=st["H"], W=st["W"], G=st["G"], D=D, softmax=softmax)
         y_ref, y_abs = oracle.forward(g, st["x_cpu"][:1], st["om_cpu"][:1], with_abs=True)
         errs = {"y": oracle.abs_scaled_error(st["y"][:1].cpu(), y_ref, y_abs)}
         if cfg["backward"]:
@@ -451,7 +458,7 @@ def _verify(cfg, stages, images):
             "pass": bool(worst <= tol), "per_stage": out}
 
 
-def _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist):
+def _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist, sm=False):
     """N > 1: gather (NCCL) every rank's first-image y and grad_offset_mask to rank 0, which
     recomputes those images alone and requires bit-identical results (forward and
     grad_offset_mask do not depend on the batch partition, R14)."""
@@ -473,9 +480,9 @@ def _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist):
                                             27 * st["G"], cfg["dtype"], images=[n])
                 x, om, gy = x.to(dev), om.to(dev), gy.to(dev)
                 if key == "y":
-                    ref = pkg.forward(x, om, group=st["G"])
+                    ref = pkg.forward(x, om, group=st["G"], softmax=sm)
                 else:
-                    ref = pkg.backward(x, om, gy, group=st["G"])[1]
+                    ref = pkg.backward(x, om, gy, group=st["G"], softmax=sm)[1]
                 ok = ok and bool(torch.equal(ref, got[r]))
     return {"cross_rank_bitexact": ok, "ranks": ws} if rank == 0 else None
 
@@ -501,12 +508,12 @@ def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
         for st, h in zip(stages, host):
             st["x"].copy_(h["x"], non_blocking=True)
             st["om"].copy_(h["om"], non_blocking=True)
-            pkg.forward(st["x"], st["om"], group=st["G"], out=st["y"])
+            pkg.forward(st["x"], st["om"], group=st["G"], softmax=args.softmax, out=st["y"])
             h["y"].copy_(st["y"], non_blocking=True)
             if cfg["backward"]:
                 st["gy"].copy_(h["gy"], non_blocking=True)
-                pkg.backward(st["x"], st["om"], st["gy"], group=st["G"], grad_input=st["gx"],
-                             grad_offset_mask=st["gom"], workspace=st["ws"])
+                pkg.backward(st["x"], st["om"], st["gy"], group=st["G"], softmax=args.softmax,
+                             grad_input=st["gx"], grad_offset_mask=st["gom"], workspace=st["ws"])
                 h["gx"].copy_(st["gx"], non_blocking=True)
                 h["gom"].copy_(st["gom"], non_blocking=True)
 
