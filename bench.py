@@ -234,6 +234,8 @@ def main():
     ap.add_argument("--offsets", default="u2", choices=["u2", "zero", "u8", "smooth"])
     ap.add_argument("--softmax", action="store_true",
                     help="DCNv3 mode (softmax over K, NEXT-1) instead of DCNv4")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bit-reproducible grad_input (int64 fixed point, NEXT-4)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -273,7 +275,8 @@ def main():
         if cfg["backward"]:
             st["gx"] = torch.empty_like(st["x"])
             st["gom"] = torch.empty_like(st["om"])
-            need = pkg.workspace_bytes(pkg.make_params(n_img, H, W, G, D), tdt)
+            need = pkg.workspace_bytes(pkg.make_params(n_img, H, W, G, D,
+                                                       deterministic=args.deterministic), tdt)
             st["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         stages.append(st)
 
@@ -285,7 +288,7 @@ def main():
         if cfg["backward"]:
             out.append(("bwd", lambda st=st: pkg.backward(
                 st["x"], st["om"], st["gy"], group=st["G"], softmax=sm, grad_input=st["gx"],
-                grad_offset_mask=st["gom"], workspace=st["ws"])))
+                grad_offset_mask=st["gom"], workspace=st["ws"], deterministic=args.deterministic)))
         return out
 
     step_calls = [(si, kind, fn) for si, st in enumerate(stages) for kind, fn in calls(st)]
@@ -397,7 +400,9 @@ def main():
         cpu = cpu_baseline(cfg)
 
     n_ours = (2 if cfg["backward"] else 1) * len(stages)
-    if cfg["backward"] and cfg["dtype"] != "f32":
+    if cfg["backward"] and args.deterministic:
+        n_ours += 2 * len(stages)  # per-image maxima + int64 -> T conversion
+    elif cfg["backward"] and cfg["dtype"] != "f32":
         n_ours += len(stages)  # fp32 -> half grad_input conversion
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "imgs/s", "n_gpus": ws,
@@ -408,6 +413,8 @@ def main():
                    "per_gpu_batch": n_img, "stages": [f"{h}x{w}x{g * D} G{g}" for h, w, g in cfg["stages"]],
                    "D": D, "kernel": "3x3 s1 p1 d1", "offset_scale": 1.0, "offsets": args.offsets,
                    "operator": "DCNv3 (softmax over K)" if sm else "DCNv4",
+                   "grad_input": ("deterministic int64 fixed point" if args.deterministic
+                                  else "fp32 atomics") if cfg["backward"] else None,
                    "parallelism": f"batch-sharded dp{ws}" if cfg["shard"] else f"replicas x{ws}",
                    "l2": f"inputs larger than L2: per-rank working set "
                          f"{sum(_alg_bytes(s['x'], s['om'], cfg['backward']) for s in stages) / 1e9:.2f} GB "
@@ -416,10 +423,13 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": n_ours * args.steps,
-        "gpu_launch_detail": f"per step: {len(stages)} fwd_kernel"
-                             + (f" + {len(stages)} bwd_kernel + {len(stages)} grad_input "
+        "gpu_launch_detail": f"per step: {len(stages)} fwd33_kernel"
+                             + (f" + {len(stages)} bwd33_kernel + {len(stages)} accumulator "
                                 f"zero-fill (cudaMemsetAsync)" if cfg["backward"] else "")
-                             + (f" + {len(stages)} convert_kernel" if cfg["backward"] and cfg["dtype"] != "f32" else ""),
+                             + (f" + {len(stages)} det_scale_kernel + {len(stages)} det_convert_kernel"
+                                if cfg["backward"] and args.deterministic else
+                                f" + {len(stages)} convert_kernel" if cfg["backward"] and cfg["dtype"] != "f32"
+                                else ""),
         "clocks": clocks,
         "stages": table,
         "parity": verify,
@@ -513,7 +523,8 @@ def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
             if cfg["backward"]:
                 st["gy"].copy_(h["gy"], non_blocking=True)
                 pkg.backward(st["x"], st["om"], st["gy"], group=st["G"], softmax=args.softmax,
-                             grad_input=st["gx"], grad_offset_mask=st["gom"], workspace=st["ws"])
+                             grad_input=st["gx"], grad_offset_mask=st["gom"], workspace=st["ws"],
+                             deterministic=args.deterministic)
                 h["gx"].copy_(st["gx"], non_blocking=True)
                 h["gom"].copy_(st["gom"], non_blocking=True)
 

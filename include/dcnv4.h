@@ -54,7 +54,7 @@ extern "C" {
 #define DCNV4_API
 #endif
 
-#define DCNV4_VERSION 100 /* 1.0.0 */
+#define DCNV4_VERSION 110 /* 1.1.0: dcnv4_params.deterministic */
 
 typedef enum { DCNV4_F32 = 0, DCNV4_F16 = 1, DCNV4_BF16 = 2 } dcnv4_dtype;
 
@@ -80,6 +80,14 @@ typedef struct {
   int32_t om_stride;     /* S, channels per offset_mask pixel; 0 => 3*G*K              */
   int32_t softmax;       /* 0 = DCNv4 (raw m, the paper's operator);
                             1 = DCNv3 normalisation, m <- softmax_K(m)         */
+  int32_t deterministic; /* backward only. 0 = grad_input summed with fp32 atomics
+                            (run-to-run differences at rounding level);
+                            1 = bit-reproducible grad_input: every contribution is
+                            rounded once to a per-image fixed-point grid 2^-F and summed
+                            in int64, F from the image's max|gy| and max|m| (DESIGN.md
+                            R19).  Adds |error| <= n * 2^-(F+1) for an element with n
+                            contributions; an image whose max|gy| or max|m| is
+                            non-finite or outside [2^-64, 2^64) gets NaN grad_input.   */
 } dcnv4_params;
 
 /* Library version (DCNV4_VERSION). */
@@ -98,7 +106,8 @@ DCNV4_API int dcnv4_forward(const dcnv4_params *p, dcnv4_dtype dtype, const void
                   const void *offset_mask, void *output, void *stream);
 
 /* Workspace bytes dcnv4_backward needs: 0 for DCNV4_F32; N*H*W*C*4 (an fp32
- * grad_input accumulator) for DCNV4_F16 / DCNV4_BF16.                                 */
+ * grad_input accumulator) for DCNV4_F16 / DCNV4_BF16; with deterministic = 1, for every
+ * dtype, N*H*W*C*8 (int64 accumulator) + 8*N rounded up to 16 (per-image maxima).     */
 DCNV4_API size_t dcnv4_backward_workspace_bytes(const dcnv4_params *p, dcnv4_dtype dtype);
 
 /* Backward of Eq. (1) given grad_output gy [N][Ho][Wo][C]:
@@ -109,10 +118,13 @@ DCNV4_API size_t dcnv4_backward_workspace_bytes(const dcnv4_params *p, dcnv4_dty
  *     padding channels [3GK, S) are written 0.
  * Both outputs are fully overwritten (nothing accumulates into caller data).
  * grad_offset_mask is bit-deterministic; grad_input is summed with fp32 atomics and is
- * deterministic only up to rounding order.  workspace: >= the size returned by
+ * deterministic only up to rounding order, unless p->deterministic = 1 (bit-identical
+ * across runs, grids and batch splits).  workspace: >= the size returned by
  * dcnv4_backward_workspace_bytes, 16-B aligned, scratch owned by the caller (may be NULL
  * when that size is 0).  Launches: a memset of the fp32 accumulator, the backward
- * kernel, and (half dtypes) one fp32 -> T conversion kernel.                          */
+ * kernel, and (half dtypes) one fp32 -> T conversion kernel; deterministic = 1: a
+ * memset of the workspace, a per-image maxima kernel, the backward kernel and one
+ * int64 -> T conversion kernel.                                                        */
 DCNV4_API int dcnv4_backward(const dcnv4_params *p, dcnv4_dtype dtype, const void *input,
                    const void *offset_mask, const void *grad_output, void *grad_input,
                    void *grad_offset_mask, void *workspace, size_t workspace_bytes,

@@ -41,7 +41,7 @@ class Params(ctypes.Structure):
                 ("pad_h", ctypes.c_int32), ("pad_w", ctypes.c_int32),
                 ("dilation_h", ctypes.c_int32), ("dilation_w", ctypes.c_int32),
                 ("offset_scale", ctypes.c_float), ("om_stride", ctypes.c_int32),
-                ("softmax", ctypes.c_int32)]
+                ("softmax", ctypes.c_int32), ("deterministic", ctypes.c_int32)]
 
 
 _lib = None
@@ -77,13 +77,13 @@ def _pair(v):
 
 
 def make_params(N, H, W, G, D, kernel_size=3, stride=1, pad=1, dilation=1, offset_scale=1.0,
-                om_stride=0, softmax=False) -> Params:
+                om_stride=0, softmax=False, deterministic=False) -> Params:
     kh, kw = _pair(kernel_size)
     sh, sw = _pair(stride)
     ph, pw = _pair(pad)
     dh, dw = _pair(dilation)
     return Params(N, H, W, G, D, kh, kw, sh, sw, ph, pw, dh, dw, float(offset_scale),
-                  int(om_stride), int(bool(softmax)))
+                  int(om_stride), int(bool(softmax)), int(bool(deterministic)))
 
 
 def _check(rc: int):
@@ -120,14 +120,14 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 def _params_for(x: torch.Tensor, om: torch.Tensor, G: int, kernel_size, stride, pad, dilation,
-                offset_scale, softmax) -> Params:
+                offset_scale, softmax, deterministic=False) -> Params:
     if x.dim() != 4 or om.dim() != 4:
         raise ValueError("x must be [N,H,W,C] and offset_mask [N,Ho,Wo,S]")
     N, H, W, C = x.shape
     if C % G:
         raise ValueError(f"C = {C} is not divisible by group = {G}")
     p = make_params(N, H, W, G, C // G, kernel_size, stride, pad, dilation, offset_scale,
-                    om.shape[3], softmax)
+                    om.shape[3], softmax, deterministic)
     Ho, Wo = output_size(p)
     if tuple(om.shape[:3]) != (N, Ho, Wo):
         raise ValueError(f"offset_mask is {tuple(om.shape)}, expected [{N}, {Ho}, {Wo}, S]")
@@ -173,11 +173,12 @@ def backward(x: torch.Tensor, offset_mask: torch.Tensor, grad_output: torch.Tens
              kernel_size=3, stride=1, pad=1, dilation=1, offset_scale=1.0, softmax=False,
              grad_input: Optional[torch.Tensor] = None,
              grad_offset_mask: Optional[torch.Tensor] = None,
-             workspace: Optional[torch.Tensor] = None):
-    """(grad_input, grad_offset_mask): one dcnv4_backward call on the current stream."""
+             workspace: Optional[torch.Tensor] = None, deterministic=False):
+    """(grad_input, grad_offset_mask): one dcnv4_backward call on the current stream.
+    deterministic=True: bit-reproducible grad_input (int64 fixed point, R19)."""
     _check_tensors(x, offset_mask, grad_output)
     p = _params_for(x, offset_mask, group, kernel_size, stride, pad, dilation, offset_scale,
-                    softmax)
+                    softmax, deterministic)
     if grad_input is None:
         grad_input = torch.empty_like(x)
     if grad_offset_mask is None:
@@ -198,8 +199,9 @@ class DCNv4Function(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, offset_mask, group, kernel_size, stride, pad, dilation, offset_scale,
-                softmax):
+                softmax, deterministic=False):
         ctx.cfg = (group, kernel_size, stride, pad, dilation, offset_scale, softmax)
+        ctx.deterministic = bool(deterministic)
         ctx.save_for_backward(x, offset_mask)
         return forward(x, offset_mask, group, kernel_size, stride, pad, dilation, offset_scale,
                        softmax)
@@ -207,12 +209,13 @@ class DCNv4Function(torch.autograd.Function):
     @staticmethod
     def backward(ctx, gy):
         x, om = ctx.saved_tensors
-        gx, gom = backward(x, om, gy.contiguous(), *ctx.cfg)
-        return gx, gom, None, None, None, None, None, None, None
+        gx, gom = backward(x, om, gy.contiguous(), *ctx.cfg, deterministic=ctx.deterministic)
+        return gx, gom, None, None, None, None, None, None, None, None
 
 
 def dcnv4(x, offset_mask, group, kernel_size=3, stride=1, pad=1, dilation=1, offset_scale=1.0,
-          softmax=False):
-    """Differentiable DCNv4 spatial aggregation (the paper's core operator)."""
+          softmax=False, deterministic=False):
+    """Differentiable DCNv4 spatial aggregation (the paper's core operator).
+    deterministic=True makes the backward's grad_input bit-reproducible."""
     return DCNv4Function.apply(x, offset_mask, group, kernel_size, stride, pad, dilation,
-                               offset_scale, softmax)
+                               offset_scale, softmax, deterministic)

@@ -70,6 +70,8 @@ int validate_geometry(const dcnv4_params* p, int dtype, int64_t* Ho, int64_t* Wo
     return fail(DCNV4_ERR_INVALID_ARG, "offset_scale is not finite");
   if (p->softmax != 0 && p->softmax != 1)
     return fail(DCNV4_ERR_INVALID_ARG, "softmax flag %d is not 0 or 1", p->softmax);
+  if (p->deterministic != 0 && p->deterministic != 1)
+    return fail(DCNV4_ERR_INVALID_ARG, "deterministic flag %d is not 0 or 1", p->deterministic);
   const int64_t K = (int64_t)p->kernel_h * p->kernel_w;
   if (K > kMaxK)
     return fail(DCNV4_ERR_UNSUPPORTED, "K = kernel_h*kernel_w = %lld exceeds %d", (long long)K, kMaxK);
@@ -492,6 +494,14 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
   g->dbg = dbg ? atoi(dbg) : 0;
   const char* np = getenv("DCNV4_NONPERSISTENT");
   lc->persistent = !(np && *np == '1');
+  lc->det = pass == 1 && p->deterministic;
+  {  // ceil(log2(Ho*Wo*K)): bound on the contributions one input element receives
+    const long long cnt = (long long)Ho * Wo * K;
+    int lcnt = 0;
+    while ((1LL << lcnt) < cnt) ++lcnt;
+    g->det_lc = lcnt;
+  }
+  g->detmax = nullptr;
   return DCNV4_OK;
 }
 
@@ -576,8 +586,11 @@ int dcnv4_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input,
 size_t dcnv4_backward_workspace_bytes(const dcnv4_params* p, dcnv4_dtype dtype) {
   int64_t Ho, Wo;
   if (validate_geometry(p, dtype, &Ho, &Wo)) return 0;
+  const size_t nelem = (size_t)p->N * p->H * p->W * p->G * p->D;
+  if (p->deterministic)  // int64 accumulator + per-image {max|gy|, max|m|}
+    return nelem * sizeof(long long) + (((size_t)p->N * 2 * sizeof(unsigned) + 15) & ~(size_t)15);
   if (dtype == DCNV4_F32) return 0;
-  return (size_t)p->N * p->H * p->W * p->G * p->D * sizeof(float);
+  return nelem * sizeof(float);
 }
 
 int dcnv4_backward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input,
@@ -614,8 +627,47 @@ int dcnv4_backward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input,
   if (rc) return rc;
   lc.stream = static_cast<cudaStream_t>(stream);
   const size_t nelem = (size_t)p->N * p->H * p->W * p->G * p->D;
+  const int K = p->kernel_h * p->kernel_w;
+  const int S = p->om_stride ? p->om_stride : 3 * p->G * K;
+  cudaError_t e;
+  if (p->deterministic) {
+    // int64 fixed point (R19): maxima pass, backward, int64 -> T conversion
+    long long* acc = static_cast<long long*>(workspace);
+    unsigned* mx = reinterpret_cast<unsigned*>(acc + nelem);
+    g.detmax = mx;
+    e = cudaMemsetAsync(workspace, 0, need, lc.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dcnv4_backward zero workspace");
+    const int npix = (int)(Ho * Wo), C = p->G * p->D;
+    switch (dtype) {
+      case DCNV4_F32:
+        e = dcnv4::launch_detmax_f32(grad_output, offset_mask, p->N, npix, C, S, p->G, K, p->softmax, mx, lc.stream);
+        break;
+      case DCNV4_F16:
+        e = dcnv4::launch_detmax_f16(grad_output, offset_mask, p->N, npix, C, S, p->G, K, p->softmax, mx, lc.stream);
+        break;
+      default:
+        e = dcnv4::launch_detmax_bf16(grad_output, offset_mask, p->N, npix, C, S, p->G, K, p->softmax, mx, lc.stream);
+        break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "dcnv4_backward maxima");
+    switch (dtype) {
+      case DCNV4_F32: e = dcnv4::launch_bwd_f32(lc, g, input, offset_mask, grad_output, acc, grad_offset_mask); break;
+      case DCNV4_F16: e = dcnv4::launch_bwd_f16(lc, g, input, offset_mask, grad_output, acc, grad_offset_mask); break;
+      default: e = dcnv4::launch_bwd_bf16(lc, g, input, offset_mask, grad_output, acc, grad_offset_mask); break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "dcnv4_backward launch");
+    const long long per_image = (long long)p->H * p->W * C;
+    const long long nchunk = (long long)(nelem * elem_size(dtype) / 16);
+    switch (dtype) {
+      case DCNV4_F32: e = dcnv4::launch_detconv_f32(acc, mx, g.det_lc, per_image, grad_input, nchunk, lc.stream); break;
+      case DCNV4_F16: e = dcnv4::launch_detconv_f16(acc, mx, g.det_lc, per_image, grad_input, nchunk, lc.stream); break;
+      default: e = dcnv4::launch_detconv_bf16(acc, mx, g.det_lc, per_image, grad_input, nchunk, lc.stream); break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "dcnv4_backward convert");
+    return DCNV4_OK;
+  }
   float* gx32 = dtype == DCNV4_F32 ? static_cast<float*>(grad_input) : static_cast<float*>(workspace);
-  cudaError_t e = cudaMemsetAsync(gx32, 0, nelem * sizeof(float), lc.stream);
+  e = cudaMemsetAsync(gx32, 0, nelem * sizeof(float), lc.stream);
   if (e != cudaSuccess) return cuda_fail(e, "dcnv4_backward zero grad_input");
   switch (dtype) {
     case DCNV4_F32:

@@ -54,36 +54,48 @@ static cudaError_t fwd_variant(const Launch& lc, const Geo& g, const void* x, co
 
 template <typename T, int NCH, int CPL>
 static cudaError_t bwd_variant(const Launch& lc, const Geo& g, const void* x, const void* om,
-                               const void* gy, float* gx32, void* gom) {
+                               const void* gy, void* gxacc, void* gom) {
   const T* xp = static_cast<const T*>(x);
   const T* op = static_cast<const T*>(om);
   const T* gyp = static_cast<const T*>(gy);
   T* gomp = static_cast<T*>(gom);
   if (lc.halo) {  // 3x3 / stride 1 / dilation 1: TMA halo + binned scatter
     void (*hk)(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, Geo,
-               const T*, const T*, float*, T*);
-    if (lc.unit) hk = bwd33_kernel<T, NCH, CPL, true>;
-    else hk = bwd33_kernel<T, NCH, CPL, false>;
+               const T*, const T*, void*, T*);
+    if (lc.det) hk = lc.unit ? bwd33_kernel<T, NCH, CPL, true, true> : bwd33_kernel<T, NCH, CPL, false, true>;
+    else hk = lc.unit ? bwd33_kernel<T, NCH, CPL, true, false> : bwd33_kernel<T, NCH, CPL, false, false>;
     if (lc.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)lc.smem);
       if (e != cudaSuccess) return e;
     }
     hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(lc.xmap, lc.gymap, g, xp,
-                                                                            op, gx32, gomp);
+                                                                            op, gxacc, gomp);
     return cudaGetLastError();
   }
-  void (*kern)(Geo, const T*, const T*, const T*, float*, T*);
-  if (lc.k33 && lc.unit) kern = bwd_kernel<T, NCH, CPL, 3, 3, true>;
-  else if (lc.k33) kern = bwd_kernel<T, NCH, CPL, 3, 3, false>;
-  else kern = bwd_kernel<T, NCH, CPL, 0, 0, false>;
+  void (*kern)(Geo, const T*, const T*, const T*, void*, T*);
+  if (lc.det) {
+    if (lc.k33 && lc.unit) kern = bwd_kernel<T, NCH, CPL, 3, 3, true, true>;
+    else if (lc.k33) kern = bwd_kernel<T, NCH, CPL, 3, 3, false, true>;
+    else kern = bwd_kernel<T, NCH, CPL, 0, 0, false, true>;
+  } else {
+    if (lc.k33 && lc.unit) kern = bwd_kernel<T, NCH, CPL, 3, 3, true, false>;
+    else if (lc.k33) kern = bwd_kernel<T, NCH, CPL, 3, 3, false, false>;
+    else kern = bwd_kernel<T, NCH, CPL, 0, 0, false, false>;
+  }
   if (lc.smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)lc.smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<grid_size(lc, (const void*)kern), lc.threads, lc.smem, lc.stream>>>(g, xp, op, gyp, gx32, gomp);
+  kern<<<grid_size(lc, (const void*)kern), lc.threads, lc.smem, lc.stream>>>(g, xp, op, gyp, gxacc, gomp);
   return cudaGetLastError();
+}
+
+static inline unsigned flat_blocks(long long n) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148LL * 16) blocks = 148LL * 16;
+  return (unsigned)(blocks < 1 ? 1 : blocks);
 }
 
 #define DCNV4_TABLE(FN, T, ...)                                        \
@@ -99,6 +111,45 @@ static cudaError_t bwd_variant(const Launch& lc, const Geo& g, const void* x, co
     case 1602: return FN<T, 16, 2>(lc, g, __VA_ARGS__);                \
     case 1604: return FN<T, 16, 4>(lc, g, __VA_ARGS__);                \
     default: return cudaErrorInvalidConfiguration;                     \
+  }
+
+// One storage type's launchers (used by dcnv4_f32.cu / _f16.cu / _bf16.cu).
+#define DCNV4_DEFINE(SUFFIX, T)                                                                 \
+  cudaError_t launch_fwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x, const void* om, \
+                                  void* y) {                                                    \
+    DCNV4_TABLE(fwd_variant, T, x, om, y)                                                      \
+  }                                                                                             \
+  cudaError_t launch_bwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x, const void* om, \
+                                  const void* gy, void* gxacc, void* gom) {                     \
+    DCNV4_TABLE(bwd_variant, T, x, om, gy, gxacc, gom)                                         \
+  }                                                                                             \
+  cudaError_t launch_convert_##SUFFIX(const float* src, void* dst, long long nchunk,            \
+                                      cudaStream_t stream) {                                    \
+    if (nchunk <= 0) return cudaSuccess;                                                        \
+    convert_kernel<T><<<flat_blocks(nchunk), 256, 0, stream>>>(src, static_cast<T*>(dst), nchunk); \
+    return cudaGetLastError();                                                                  \
+  }                                                                                             \
+  cudaError_t launch_detmax_##SUFFIX(const void* gy, const void* om, long long N, int npix,     \
+                                     int C, int S, int G, int K, int softmax, unsigned* mx,     \
+                                     cudaStream_t stream) {                                     \
+    if (N <= 0) return cudaSuccess;                                                             \
+    const long long chunks = (long long)npix * C / Elem<T>::E;                                 \
+    long long per = (chunks + 255) / 256;                                                      \
+    const long long want = (148LL * 8 + N - 1) / N;                                            \
+    if (per > want) per = want;                                                                 \
+    dim3 grid((unsigned)(per < 1 ? 1 : per), (unsigned)N);                                      \
+    det_scale_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(gy),                   \
+                                                  static_cast<const T*>(om), chunks, npix, S, G, K, \
+                                                  softmax, mx);                                 \
+    return cudaGetLastError();                                                                  \
+  }                                                                                             \
+  cudaError_t launch_detconv_##SUFFIX(const long long* src, const unsigned* mx, int lc,         \
+                                      long long per_image, void* dst, long long nchunk,         \
+                                      cudaStream_t stream) {                                    \
+    if (nchunk <= 0) return cudaSuccess;                                                        \
+    det_convert_kernel<T><<<flat_blocks(nchunk), 256, 0, stream>>>(src, mx, lc, per_image,     \
+                                                                  static_cast<T*>(dst), nchunk); \
+    return cudaGetLastError();                                                                  \
   }
 
 }  // namespace dcnv4

@@ -3,23 +3,6 @@
 
 namespace dcnv4 {
 
-cudaError_t launch_fwd_f16(const Launch& lc, const Geo& g, const void* x, const void* om,
-                          void* y) {
-  DCNV4_TABLE(fwd_variant, __half, x, om, y)
-}
-
-cudaError_t launch_bwd_f16(const Launch& lc, const Geo& g, const void* x, const void* om,
-                          const void* gy, float* gx32, void* gom) {
-  DCNV4_TABLE(bwd_variant, __half, x, om, gy, gx32, gom)
-}
-
-cudaError_t launch_convert_f16(const float* src, void* dst, long long nchunk,
-                              cudaStream_t stream) {
-  if (nchunk <= 0) return cudaSuccess;
-  long long blocks = (nchunk + 255) / 256;
-  if (blocks > 148LL * 16) blocks = 148LL * 16;
-  convert_kernel<__half><<<(unsigned)blocks, 256, 0, stream>>>(src, static_cast<__half*>(dst), nchunk);
-  return cudaGetLastError();
-}
+DCNV4_DEFINE(f16, __half)
 
 }  // namespace dcnv4

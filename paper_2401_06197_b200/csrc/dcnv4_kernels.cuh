@@ -62,6 +62,10 @@ struct Geo {
   int gy_box_bytes;
   int o_gy, o_om, o_gom, o_cnt, o_slot, o_ent, o_wsum, o_bar;
   int dbg;  // profiling only (env DCNV4_DBG): bit0 skips the grad_input phases P2-P4
+  // deterministic grad_input (params.deterministic): ceil(log2(Ho*Wo*K)) and the
+  // per-image maxima {max|gy|, max|m|} (float bits) written by det_scale_kernel
+  int det_lc;
+  const unsigned* detmax;
 };
 
 // ------------------------------------------------------------------ element types
@@ -165,6 +169,44 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
+
+// ------------------------------------------------------------------ deterministic grad_input
+// DESIGN.md R19.  Every contribution m*w*gy_c of image n is rounded once to the integer
+// grid 2^-F_n and summed in int64 (shared-memory bins and global reductions alike), so
+// the sum is independent of the order the atomics land in.  F_n is fixed per image from
+// M_g = max|gy|, M_m = max|m| and lc = ceil(log2(Ho*Wo*K)) (an input element receives at
+// most Ho*Wo*K contributions, each < 2^eg * 2^em):  F = 62 - lc - eg - em, so every
+// partial sum stays below 2^62.  Images whose maxima are non-finite or outside
+// [2^-64, 2^64) are flagged and their grad_input is written as NaN.
+struct DetScale {
+  float s1, s2;  // 2^F = s1 * s2 (each a normal float)
+  int F;
+  bool bad;
+};
+
+__device__ __forceinline__ int det_exp(unsigned bits) {  // smallest e with |v| < 2^e
+  const int E = (int)(bits >> 23);
+  return (E < 1 ? 1 : E) - 126;
+}
+
+__device__ __forceinline__ DetScale det_scale(const unsigned* mx, int n, int lc) {
+  DetScale d = {0.f, 0.f, 0, false};
+  const unsigned gb = mx[2 * n], mb = mx[2 * n + 1];
+  if (gb >= 0x7f800000u || mb >= 0x7f800000u) { d.bad = true; return d; }
+  if (gb == 0u || mb == 0u) return d;  // every contribution is exactly 0
+  const int eg = det_exp(gb), em = det_exp(mb);
+  if (eg < -63 || eg > 64 || em < -63 || em > 64) { d.bad = true; return d; }
+  d.F = 62 - lc - eg - em;  // in [-66 - lc, 188 - lc]
+  const int F1 = d.F / 2, F2 = d.F - F1;
+  d.s1 = __int_as_float((F1 + 127) << 23);
+  d.s2 = __int_as_float((F2 + 127) << 23);
+  return d;
+}
+
+// 64-bit integer reduction (RED.E.ADD.64): order-independent
+__device__ __forceinline__ void red_add_s64(long long* p, long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
@@ -729,12 +771,14 @@ __global__ void __launch_bounds__(256) fwd33_kernel(const __grid_constant__ CUte
 //   grad_dx partial = (1-fy)(S_1 - S_0) + fy (S_3 - S_2)     [times s*m]
 // (S_q of out-of-image corners is 0) reduced over the L lanes with shuffles;
 // grad_input += m w_q gy by 16-B vector reductions.
-template <typename T, int NCH, int CPL, int KH, int KW, bool UNIT>
+template <typename T, int NCH, int CPL, int KH, int KW, bool UNIT, bool DET>
 __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x,
                                                   const T* __restrict__ om,
                                                   const T* __restrict__ gy,
-                                                  float* __restrict__ gx32,
+                                                  void* __restrict__ gxacc,
                                                   T* __restrict__ gom) {
+  float* const gx32 = static_cast<float*>(gxacc);       // DET = false
+  long long* const gx64 = static_cast<long long*>(gxacc);  // DET = true
   constexpr int L = NCH / CPL;
   constexpr int E = Elem<T>::E;
   constexpr int KC = KH * KW;
@@ -774,8 +818,15 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x
     const long long img = (long long)tl.n * H * W * C;
     const T* xh[CPL];
     float* gxh[CPL];
+    long long* gxq[CPL];
 #pragma unroll
-    for (int h = 0; h < CPL; ++h) { xh[h] = x + img + sl.co[h]; gxh[h] = gx32 + img + sl.co[h]; }
+    for (int h = 0; h < CPL; ++h) {
+      xh[h] = x + img + sl.co[h];
+      gxh[h] = gx32 + img + sl.co[h];
+      gxq[h] = gx64 + img + sl.co[h];
+    }
+    DetScale ds = {0.f, 0.f, 0, false};
+    if constexpr (DET) ds = det_scale(g.detmax, tl.n, g.det_lc);
 
     float gyv[CPL * E];
     {
@@ -813,12 +864,20 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x
       for (int q = 0; q < 4; ++q) {
         const float a = m * c.w[q];
         if (active && a != 0.f) {
+          if constexpr (DET) {
+            const float ap = (a * ds.s1) * ds.s2;
 #pragma unroll
-          for (int h = 0; h < CPL; ++h) {
+            for (int h = 0; h < CPL; ++h)
 #pragma unroll
-            for (int e = 0; e < E; e += 4)
-              red_add_v4_idx(gxh[h] + e, c.o[q], a * gyv[h * E + e], a * gyv[h * E + e + 1],
-                             a * gyv[h * E + e + 2], a * gyv[h * E + e + 3]);
+              for (int e = 0; e < E; ++e) red_add_s64(gxq[h] + c.o[q] + e, __float2ll_rn(ap * gyv[h * E + e]));
+          } else {
+#pragma unroll
+            for (int h = 0; h < CPL; ++h) {
+#pragma unroll
+              for (int e = 0; e < E; e += 4)
+                red_add_v4_idx(gxh[h] + e, c.o[q], a * gyv[h * E + e], a * gyv[h * E + e + 1],
+                               a * gyv[h * E + e + 2], a * gyv[h * E + e + 3]);
+            }
           }
         }
       }
@@ -951,13 +1010,15 @@ __device__ __forceinline__ int block_exclusive_scan(int* data, int n, int* warp_
   return total;
 }
 
-template <typename T, int NCH, int CPL, bool UNIT>
+template <typename T, int NCH, int CPL, bool UNIT, bool DET>
 __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUtensorMap xmap,
                                                     const __grid_constant__ CUtensorMap gymap, Geo g,
                                                     const T* __restrict__ x,
                                                     const T* __restrict__ om,
-                                                    float* __restrict__ gx32,
+                                                    void* __restrict__ gxacc,
                                                     T* __restrict__ gom) {
+  float* const gx32 = static_cast<float*>(gxacc);       // DET = false
+  long long* const gx64 = static_cast<long long*>(gxacc);  // DET = true
   constexpr int L = NCH / CPL;
   constexpr int E = Elem<T>::E;
   constexpr int GC = NCH >= 8 ? 1 : 8 / NCH;
@@ -1014,6 +1075,8 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       n = (int)q3;
     }
     const int hy0 = h0 - g.ph - 2, hx0 = w0 - g.pw - 2;  // halo origin in input pixels
+    DetScale ds = {0.f, 0.f, 0, false};
+    if constexpr (DET) ds = det_scale(g.detmax, n, g.det_lc);
     // ---- P0: loads
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1123,6 +1186,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       if (outside) {  // rare: samples beyond the halo -- global gathers and reductions
         const T* ximg = x + (long long)n * H * W * C;
         float* gximg = gx32 + (long long)n * H * W * C;
+        long long* gxqimg = gx64 + (long long)n * H * W * C;
         const unsigned gbase = (g0 + gl) * DG;
         float smx = 0.f, sinv = 1.f;
         if (g.softmax) softmax_stats<T>(row, K, smx, sinv);
@@ -1149,13 +1213,23 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           for (int q = 0; q < 4; ++q) {
             if (!c.ok[q]) S[q] = 0.f;
             const float a = mk * c.w[q];
-            if (a != 0.f)
+            if (a != 0.f) {
+              if constexpr (DET) {
+                const float ap = (a * ds.s1) * ds.s2;
 #pragma unroll
-              for (int h = 0; h < CPL; ++h)
+                for (int h = 0; h < CPL; ++h)
 #pragma unroll
-                for (int e = 0; e < E; e += 4)
-                  red_add_v4_idx(gximg + co[h] + e, c.o[q], a * gyv[h * E + e], a * gyv[h * E + e + 1],
-                                 a * gyv[h * E + e + 2], a * gyv[h * E + e + 3]);
+                  for (int e = 0; e < E; ++e)
+                    red_add_s64(gxqimg + c.o[q] + co[h] + e, __float2ll_rn(ap * gyv[h * E + e]));
+              } else {
+#pragma unroll
+                for (int h = 0; h < CPL; ++h)
+#pragma unroll
+                  for (int e = 0; e < E; e += 4)
+                    red_add_v4_idx(gximg + co[h] + e, c.o[q], a * gyv[h * E + e], a * gyv[h * E + e + 1],
+                                   a * gyv[h * E + e + 2], a * gyv[h * E + e + 3]);
+              }
+            }
           }
           const float hy = 1.f - c.fy, hx = 1.f - c.fx;
           float sgm = c.w[0] * S[0] + c.w[1] * S[1] + c.w[2] * S[2] + c.w[3] * S[3];
@@ -1247,6 +1321,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       constexpr int PC = NCH >= 2 ? 2 : 1;
       constexpr int NCL = NCH / PC;  // lanes per (halo pixel, group)
       float* gximg = gx32 + (long long)n * H * W * C;
+      long long* gxqimg = gx64 + (long long)n * H * W * C;
       for (int f = tid; f < NT * GC * NCL; f += blockDim.x) {
         const int cl = f % NCL;
         const int gg = (f / NCL) % GC;
@@ -1258,25 +1333,49 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
         int cc[PC];
 #pragma unroll
         for (int h = 0; h < PC; ++h) cc[h] = (cl * PC + ((h + tt) & (PC - 1))) * E;
-        float acc[PC * E];
-#pragma unroll
-        for (int e = 0; e < PC * E; ++e) acc[e] = 0.f;
         const T* gyg = gyt + gg * DG;
-        for (int q = 0; q < ne; ++q) {
-          const uint2 en = b[q];
-          const T* src = gyg + en.y * (GC * DG);
+        const int yy = hy0 + tt / HWC, xx = hx0 + tt % HWC;
+        const unsigned dsto = (unsigned)(yy * W + xx) * C + (g0 + gg) * DG;
+        if constexpr (DET) {  // per-contribution rounding to the 2^-F grid, int64 sums
+          long long acc[PC * E];
+#pragma unroll
+          for (int e = 0; e < PC * E; ++e) acc[e] = 0;
+          for (int q = 0; q < ne; ++q) {
+            const uint2 en = b[q];
+            const T* src = gyg + en.y * (GC * DG);
+            const float ap = (__uint_as_float(en.x) * ds.s1) * ds.s2;
+#pragma unroll
+            for (int h = 0; h < PC; ++h) {
+              float v[E];
+              Elem<T>::unpack(*reinterpret_cast<const uint4*>(src + cc[h]), v);
+#pragma unroll
+              for (int e = 0; e < E; ++e) acc[h * E + e] += __float2ll_rn(ap * v[e]);
+            }
+          }
+          long long* dst = gxqimg + dsto;
 #pragma unroll
           for (int h = 0; h < PC; ++h)
-            fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src + cc[h]));
+#pragma unroll
+            for (int e = 0; e < E; ++e) red_add_s64(dst + cc[h] + e, acc[h * E + e]);
+        } else {
+          float acc[PC * E];
+#pragma unroll
+          for (int e = 0; e < PC * E; ++e) acc[e] = 0.f;
+          for (int q = 0; q < ne; ++q) {
+            const uint2 en = b[q];
+            const T* src = gyg + en.y * (GC * DG);
+#pragma unroll
+            for (int h = 0; h < PC; ++h)
+              fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src + cc[h]));
+          }
+          float* dst = gximg + dsto;
+#pragma unroll
+          for (int h = 0; h < PC; ++h)
+#pragma unroll
+            for (int e = 0; e < E; e += 4)
+              red_add_v4(dst + cc[h] + e, acc[h * E + e], acc[h * E + e + 1], acc[h * E + e + 2],
+                         acc[h * E + e + 3]);
         }
-        const int yy = hy0 + tt / HWC, xx = hx0 + tt % HWC;
-        float* dst = gximg + ((unsigned)(yy * W + xx) * C + (g0 + gg) * DG);
-#pragma unroll
-        for (int h = 0; h < PC; ++h)
-#pragma unroll
-          for (int e = 0; e < E; e += 4)
-            red_add_v4(dst + cc[h] + e, acc[h * E + e], acc[h * E + e + 1], acc[h * E + e + 2],
-                       acc[h * E + e + 3]);
       }
     }
     __syncthreads();  // shared memory is reused by the next tile
@@ -1296,6 +1395,68 @@ __global__ void __launch_bounds__(256) convert_kernel(const float* __restrict__ 
     for (int q = 0; q < E / 4; ++q) {
       float4 f = __ldcs(s4 + q);
       v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+    }
+    reinterpret_cast<uint4*>(dst)[i] = Elem<T>::pack(v);
+  }
+}
+
+// Deterministic mode, pass 1: per-image maxima {max|gy|, max|m|} as float bits
+// (non-negative floats order as unsigned integers; NaN sorts above +inf).  grid =
+// (blocks per image, N); mx must be zeroed.  softmax: the mask bound is 1 (softmax
+// outputs), unless a logit is non-finite.
+template <typename T>
+__global__ void __launch_bounds__(256) det_scale_kernel(const T* __restrict__ gy,
+                                                        const T* __restrict__ om, long long gy_chunks,
+                                                        int npix, int S, int G, int K, int softmax,
+                                                        unsigned* __restrict__ mx) {
+  constexpr int E = Elem<T>::E;
+  const int n = blockIdx.y;
+  const int nt = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned vg = 0u, vm = 0u;
+  const uint4* g4 = reinterpret_cast<const uint4*>(gy) + (long long)n * gy_chunks;
+  for (long long i = t0; i < gy_chunks; i += nt) {
+    float v[E];
+    Elem<T>::unpack(ld_stream(g4 + i), v);
+#pragma unroll
+    for (int e = 0; e < E; ++e) vg = max(vg, __float_as_uint(v[e]) & 0x7fffffffu);
+  }
+  const T* o = om + (long long)n * npix * S;
+  const long long nm = (long long)npix * G * K;
+  for (long long i = t0; i < nm; i += nt) {
+    const long long pix = i / (G * K);
+    const int r = (int)(i - pix * (G * K));
+    const int gg = r / K, k = r - gg * K;
+    vm = max(vm, __float_as_uint(Elem<T>::f(o[pix * S + gg * 3 * K + 2 * K + k])) & 0x7fffffffu);
+  }
+  if (softmax) vm = vm >= 0x7f800000u ? vm : 0x3f800000u;
+  vg = __reduce_max_sync(0xffffffffu, vg);
+  vm = __reduce_max_sync(0xffffffffu, vm);
+  if ((threadIdx.x & 31) == 0) {
+    if (vg) atomicMax(mx + 2 * n, vg);
+    if (vm) atomicMax(mx + 2 * n + 1, vm);
+  }
+}
+
+// Deterministic mode, pass 3: int64 accumulator -> grad_input in T (RN), NaN for flagged
+// images.  nchunk = number of E-element chunks; per_image = H*W*C.
+template <typename T>
+__global__ void __launch_bounds__(256) det_convert_kernel(const long long* __restrict__ src,
+                                                          const unsigned* __restrict__ mx, int lc,
+                                                          long long per_image, T* __restrict__ dst,
+                                                          long long nchunk) {
+  constexpr int E = Elem<T>::E;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nchunk;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)((i * E) / per_image);
+    const DetScale d = det_scale(mx, n, lc);
+    float v[E];
+    const longlong2* s2 = reinterpret_cast<const longlong2*>(src + i * E);
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) {
+      const longlong2 w = __ldcs(s2 + q);
+      v[2 * q] = d.bad ? __int_as_float(0x7fc00000) : (float)ldexp((double)w.x, -d.F);
+      v[2 * q + 1] = d.bad ? __int_as_float(0x7fc00000) : (float)ldexp((double)w.y, -d.F);
     }
     reinterpret_cast<uint4*>(dst)[i] = Elem<T>::pack(v);
   }

@@ -24,14 +24,21 @@ struct Launch {
   bool halo;        // forward: TMA halo kernel (else the global-gather kernel)
   CUtensorMap xmap; // TMA descriptor of x for the halo kernels
   CUtensorMap gymap;  // TMA descriptor of grad_output (backward halo kernel)
+  bool det;         // backward: deterministic int64 grad_input accumulation
 };
 
 #define DCNV4_DECLARE(SUFFIX)                                                              \
   cudaError_t launch_fwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x,          \
                                   const void* om, void* y);                                \
   cudaError_t launch_bwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x,          \
-                                  const void* om, const void* gy, float* gx32, void* gom); \
+                                  const void* om, const void* gy, void* gxacc, void* gom); \
   cudaError_t launch_convert_##SUFFIX(const float* src, void* dst, long long nchunk,      \
+                                      cudaStream_t stream);                                \
+  cudaError_t launch_detmax_##SUFFIX(const void* gy, const void* om, long long N, int npix, \
+                                     int C, int S, int G, int K, int softmax, unsigned* mx, \
+                                     cudaStream_t stream);                                 \
+  cudaError_t launch_detconv_##SUFFIX(const long long* src, const unsigned* mx, int lc,     \
+                                      long long per_image, void* dst, long long nchunk,     \
                                       cudaStream_t stream);
 
 DCNV4_DECLARE(f32)

@@ -69,7 +69,7 @@ def _err(gpu, ref, scale, mask=None, qfloor=0.0):
 
 
 def run_case(g: oracle.Geometry, dtype="f32", offsets="u2", images=None, backward=True,
-             inputs=None, check_images=None):
+             inputs=None, check_images=None, deterministic=False):
     """Run fwd (+bwd) on the GPU for the whole batch; compare `check_images` (default all)
     against the oracle.  Returns the dict of max errors."""
     dev = torch.device("cuda:0")
@@ -84,7 +84,7 @@ def run_case(g: oracle.Geometry, dtype="f32", offsets="u2", images=None, backwar
               dilation=(g.dh, g.dw), offset_scale=g.offset_scale, softmax=g.softmax)
     y = pkg.forward(xd, omd, **kw)
     if backward:
-        gx, gom = pkg.backward(xd, omd, gyd, **kw)
+        gx, gom = pkg.backward(xd, omd, gyd, deterministic=deterministic, **kw)
     torch.cuda.synchronize()
     sel = list(range(g.N)) if check_images is None else list(check_images)
     gs = oracle.Geometry(**{**g.__dict__, "N": len(sel)})
