@@ -376,6 +376,7 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   int seg_bytes = (segB_raw + 15) & ~15;
   if ((seg_bytes / 16) % 2 == 0) seg_bytes += 16;
   const int npix = TH * 8, HH = TH + 6, NT = HH * 14;
+  if (NT > (int)sizeof(g->p4ord)) return false;
   auto up = [](size_t v, size_t a) { return (v + a - 1) / a * a; };
   size_t o = 0;
   const int halo_box = HH * 14 * PB;
@@ -421,6 +422,31 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   g2.gy_box_bytes = gy_box;
   g2.o_gy = o_gy; g2.o_om = o_om; g2.o_gom = o_gom; g2.o_cnt = o_cnt; g2.o_slot = o_slot;
   g2.o_ent = o_ent; g2.o_wsum = o_wsum; g2.o_bar = o_bar;
+  {  // P4 bin order: expected entry count for U(-2,2)-like offsets, separable in y and x.
+    // A sample of output row py lands (floor) on halo row py + j + 2 + floor(dy), j in
+    // {0,1,2}, floor(dy) in {-2..1}; its corners cover that row and the next.
+    auto profile = [](int n_out, int n_halo, double* prof) {
+      double w[7] = {0, 0, 0, 0, 0, 0, 0};
+      for (int j = 0; j < 3; ++j)
+        for (int f = 0; f < 4; ++f) { w[j + f] += 0.5; w[j + f + 1] += 0.5; }
+      for (int r = 0; r < n_halo; ++r) {
+        prof[r] = 0;
+        for (int q = 0; q < n_out; ++q)
+          if (r - q >= 0 && r - q < 7) prof[r] += w[r - q];
+      }
+    };
+    double py_[32], px_[32];
+    profile(TH, HH, py_);
+    profile(8, 14, px_);
+    int idx[200];
+    for (int i = 0; i < NT; ++i) idx[i] = i;
+    const char* ord = getenv("DCNV4_P4ORDER");
+    if (!(ord && *ord == '0'))
+      std::stable_sort(idx, idx + NT, [&](int a, int b2) {
+        return py_[a / 14] * px_[a % 14] > py_[b2 / 14] * px_[b2 % 14];
+      });
+    for (int i = 0; i < NT; ++i) g2.p4ord[i] = (unsigned char)idx[i];
+  }
   g2.unit = unit;
   g2.upp = segB_raw / unit;
   g2.fd_gb = make_fastdiv((unsigned)gblocks);

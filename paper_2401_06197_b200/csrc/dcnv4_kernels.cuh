@@ -66,6 +66,9 @@ struct Geo {
   // per-image maxima {max|gy|, max|m|} (float bits) written by det_scale_kernel
   int det_lc;
   const unsigned* detmax;
+  // bwd33 P4: halo bins in descending order of their expected entry count (so the lanes of
+  // a warp get bins of similar size and wait less on each other); identity if disabled
+  unsigned char p4ord[200];
 };
 
 // ------------------------------------------------------------------ element types
@@ -1325,14 +1328,15 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       for (int f = tid; f < NT * GC * NCL; f += blockDim.x) {
         const int cl = f % NCL;
         const int gg = (f / NCL) % GC;
-        const int tt = f / (NCL * GC);
+        const int rk = f / (NCL * GC);
+        const int tt = g.p4ord[rk];
         const int b0 = offs[gg * NT + tt];
         const int ne = offs[gg * NT + tt + 1] - b0;
         if (ne == 0) continue;
         const uint2* b = ent + b0;
         int cc[PC];
 #pragma unroll
-        for (int h = 0; h < PC; ++h) cc[h] = (cl * PC + ((h + tt) & (PC - 1))) * E;
+        for (int h = 0; h < PC; ++h) cc[h] = (cl * PC + ((h + rk) & (PC - 1))) * E;
         const T* gyg = gyt + gg * DG;
         const int yy = hy0 + tt / HWC, xx = hx0 + tt % HWC;
         const unsigned dsto = (unsigned)(yy * W + xx) * C + (g0 + gg) * DG;
