@@ -291,7 +291,10 @@ bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   if (p->G % GC) return false;
   const int PB = GC * nch * 16;
   const int per_row = 8 * GC * L;  // threads per tile row
-  int TH = 256 / per_row;
+  // 128-thread CTAs (TH = 4 at D = 16): four CTAs per SM overlap their per-tile halo waits
+  // better than two 256-thread ones; measured best or within 2% on every c2/c3 stage
+  // (profiles/r01_fwd_th_sweep.jsonl)
+  int TH = std::max(1, 128 / per_row);
   if (TH < 1) return false;
   const char* th_env = getenv("DCNV4_FWD33_TH");
   if (th_env && *th_env) TH = std::max(1, std::min(TH, atoi(th_env)));
