@@ -974,13 +974,16 @@ __device__ __forceinline__ V pick4(const V* v, int q) {
   return (q & 2) ? hi : lo;
 }
 
+// PAD2: every count is rounded up to even (bins start 16-B aligned for paired entry loads)
+// and the parity of the true count is kept in bit 0 of the (even) offset.
+template <bool PAD2>
 __device__ __forceinline__ int block_exclusive_scan(int* data, int n, int* warp_sums) {
   // in-place exclusive prefix sum of data[0..n) by the whole CTA; returns the total
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int per = (n + nt - 1) / nt;
   const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
   int local = 0;
-  for (int i = b0; i < b1; ++i) local += data[i];
+  for (int i = b0; i < b1; ++i) local += PAD2 ? (data[i] + 1) & ~1 : data[i];
   int incl = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1005,8 +1008,8 @@ __device__ __forceinline__ int block_exclusive_scan(int* data, int n, int* warp_
   int run = warp_sums[warp] + incl - local;
   for (int i = b0; i < b1; ++i) {
     const int v = data[i];
-    data[i] = run;
-    run += v;
+    data[i] = PAD2 ? run | (v & 1) : run;
+    run += PAD2 ? (v + 1) & ~1 : v;
   }
   const int total = warp_sums[32];
   __syncthreads();
@@ -1033,6 +1036,9 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
   extern __shared__ __align__(128) unsigned char smem[];
   const int TH = g.TH, HH = TH + 6, NT = HH * HWC;
   const int npix = TH * TW;
+  // slot rows (one per (k, corner)) padded by 32 B so the two corner rows one warp store
+  // touches fall in different banks
+  const int SPS = npix * GC + 16;
   const T* gyt = reinterpret_cast<const T*>(smem + g.o_gy);
   T* const omt = reinterpret_cast<T*>(smem + g.o_om);
   float* const gomt = reinterpret_cast<float*>(smem + g.o_gom);
@@ -1182,7 +1188,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           const int q = (lg % 4) + r * L;
           if (lg < 4 && q < 4 && pick4(ok, q) && m[k] * pick4(w, q) != 0.f) {
             const int tt = (ylc + (q >> 1)) * HWC + xlc + (q & 1);
-            slots[(k * 4 + q) * (npix * GC) + item] = (unsigned short)atomicAdd(&cnt[gl * NT + tt], 1);
+            slots[(k * 4 + q) * SPS + item] = (unsigned short)atomicAdd(&cnt[gl * NT + tt], 1);
           }
         }
       }
@@ -1267,7 +1273,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
     int* const offs = cnt;
     if (g.dbg & 1) { __syncthreads(); continue; }
     {
-      const int total = block_exclusive_scan(offs, GC * NT, wsum);
+      const int total = block_exclusive_scan<true>(offs, GC * NT, wsum);
       if (tid == 0) offs[GC * NT] = total;
       __syncthreads();
     }
@@ -1298,7 +1304,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           const float a = m[k] * pick4(w, q);
           if (lg < 4 && q < 4 && pick4(ok, q) && a != 0.f) {
             const int tt = (yl + (q >> 1)) * HWC + xl + (q & 1);
-            const int e = offs[gl * NT + tt] + slots[(k * 4 + q) * (npix * GC) + item];
+            const int e = (offs[gl * NT + tt] & ~1) + slots[(k * 4 + q) * SPS + item];
             ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
           }
         }
@@ -1330,10 +1336,12 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
         const int gg = (f / NCL) % GC;
         const int rk = f / (NCL * GC);
         const int tt = g.p4ord[rk];
-        const int b0 = offs[gg * NT + tt];
-        const int ne = offs[gg * NT + tt + 1] - b0;
-        if (ne == 0) continue;
-        const uint2* b = ent + b0;
+        const int o0 = offs[gg * NT + tt];
+        const int b0 = o0 & ~1;
+        const int np = ((offs[gg * NT + tt + 1] & ~1) - b0) >> 1;  // entry pairs (last may be half)
+        if (np == 0) continue;
+        const bool odd = o0 & 1;
+        const uint4* b = reinterpret_cast<const uint4*>(ent + b0);
         int cc[PC];
 #pragma unroll
         for (int h = 0; h < PC; ++h) cc[h] = (cl * PC + ((h + rk) & (PC - 1))) * E;
@@ -1344,16 +1352,20 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           long long acc[PC * E];
 #pragma unroll
           for (int e = 0; e < PC * E; ++e) acc[e] = 0;
-          for (int q = 0; q < ne; ++q) {
-            const uint2 en = b[q];
-            const T* src = gyg + en.y * (GC * DG);
-            const float ap = (__uint_as_float(en.x) * ds.s1) * ds.s2;
+          for (int q = 0; q < np; ++q) {
+            const uint4 en = b[q];
 #pragma unroll
-            for (int h = 0; h < PC; ++h) {
-              float v[E];
-              Elem<T>::unpack(*reinterpret_cast<const uint4*>(src + cc[h]), v);
+            for (int r = 0; r < 2; ++r) {
+              if (r == 1 && odd && q == np - 1) break;
+              const T* src = gyg + (r ? en.w : en.y) * (GC * DG);
+              const float ap = (__uint_as_float(r ? en.z : en.x) * ds.s1) * ds.s2;
 #pragma unroll
-              for (int e = 0; e < E; ++e) acc[h * E + e] += __float2ll_rn(ap * v[e]);
+              for (int h = 0; h < PC; ++h) {
+                float v[E];
+                Elem<T>::unpack(*reinterpret_cast<const uint4*>(src + cc[h]), v);
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[h * E + e] += __float2ll_rn(ap * v[e]);
+              }
             }
           }
           long long* dst = gxqimg + dsto;
@@ -1365,12 +1377,27 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           float acc[PC * E];
 #pragma unroll
           for (int e = 0; e < PC * E; ++e) acc[e] = 0.f;
-          for (int q = 0; q < ne; ++q) {
-            const uint2 en = b[q];
-            const T* src = gyg + en.y * (GC * DG);
+          // full pairs (branch-free, unrolled by the compiler), then the last pair
+          for (int q = 0; q < np - 1; ++q) {
+            const uint4 en = b[q];
+            const T* src0 = gyg + en.y * (GC * DG);
+            const T* src1 = gyg + en.w * (GC * DG);
 #pragma unroll
-            for (int h = 0; h < PC; ++h)
-              fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src + cc[h]));
+            for (int h = 0; h < PC; ++h) {
+              fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src0 + cc[h]));
+              fma_chunk<T>(acc + h * E, __uint_as_float(en.z), *reinterpret_cast<const uint4*>(src1 + cc[h]));
+            }
+          }
+          {
+            const uint4 en = b[np - 1];
+            const T* src0 = gyg + en.y * (GC * DG);
+            const T* src1 = gyg + (odd ? 0u : en.w) * (GC * DG);
+            const float a1 = odd ? 0.f : __uint_as_float(en.z);
+#pragma unroll
+            for (int h = 0; h < PC; ++h) {
+              fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src0 + cc[h]));
+              fma_chunk<T>(acc + h * E, a1, *reinterpret_cast<const uint4*>(src1 + cc[h]));
+            }
           }
           float* dst = gximg + dsto;
 #pragma unroll
