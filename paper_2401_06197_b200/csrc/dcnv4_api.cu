@@ -394,7 +394,7 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   const int o_cnt = (int)o;
   o = up(o + ((size_t)GC * NT + 1) * 4, 16);
   const int o_slot = (int)o;
-  o = up(o + ((size_t)npix * GC + 16) * 36 * 2, 16);
+  o = up(o + (size_t)GC * NT * 4, 16);  // fill pointers
   const int o_ent = (int)o;
   o = up(o + ((size_t)GC * npix * 36 + (size_t)GC * NT) * 8, 16);  // + one pad slot per bin
   const int o_wsum = (int)o;

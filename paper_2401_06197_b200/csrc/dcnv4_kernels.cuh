@@ -953,13 +953,14 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x
 // ------------------------------------------------------------------ backward, 3x3 halo + binned scatter
 // One CTA tile (TH x 8 output pixels x GC groups) per iteration, persistent grid:
 //  P0  TMA: x halo ((TH+6) x 14 px) and the gy tile; cp.async: offset_mask rows
-//  P1  per (pixel, group) lane group, the 9 samples from the shared-memory halo:
+//  P1  coordinates only: every in-image corner contribution a = m*w_q (the bilinear
+//      scatter weight) is counted into its halo target bin (native shared-memory integer
+//      reduction; fp32 shared atomics would be CAS loops)
+//  P2  exclusive scan of the bin counts (padded to even: 16-B aligned bins) -> fill pointers
+//  P3  per (pixel, group) lane group, the 9 samples from the shared-memory halo:
 //        S_q = <gy, x_q> (4 dot products per sample), grad_m / grad_offset partials
-//        reduced over the L lanes -> grad_om tile; every in-image corner contribution
-//        a = m*w_q (the bilinear scatter weight) is counted into its halo target bin
-//        (native shared atomic ATOMS.ADD; fp32 shared atomics would be CAS loops)
-//  P2  exclusive scan of the bin counts
-//  P3  contributions written (a, source pixel) into their bins (counting sort)
+//        reduced over the L lanes -> grad_om tile; each contribution is filed as
+//        (a, source pixel) at its bin's fill pointer (counting sort, one ATOMS each)
 //  P4  per (halo pixel, group, 16-B chunk): gx = sum_bin a * gy[source] from shared
 //      memory, then ONE 16-B vector reduction into the fp32 grad_input accumulator --
 //      ~3x the tile's pixels instead of 36 per (pixel, group) (the v3 kernel was bound
@@ -1036,14 +1037,11 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
   extern __shared__ __align__(128) unsigned char smem[];
   const int TH = g.TH, HH = TH + 6, NT = HH * HWC;
   const int npix = TH * TW;
-  // slot rows (one per (k, corner)) padded by 32 B so the two corner rows one warp store
-  // touches fall in different banks
-  const int SPS = npix * GC + 16;
   const T* gyt = reinterpret_cast<const T*>(smem + g.o_gy);
   T* const omt = reinterpret_cast<T*>(smem + g.o_om);
   float* const gomt = reinterpret_cast<float*>(smem + g.o_gom);
   int* const cnt = reinterpret_cast<int*>(smem + g.o_cnt);
-  unsigned short* const slots = reinterpret_cast<unsigned short*>(smem + g.o_slot);
+  int* const fill = reinterpret_cast<int*>(smem + g.o_slot);  // per-bin fill pointers (P3)
   uint2* const ent = reinterpret_cast<uint2*>(smem + g.o_ent);
   int* const wsum = reinterpret_cast<int*>(smem + g.o_wsum);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + g.o_bar);
@@ -1119,12 +1117,74 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
     const bool active = slot_ok && ho < g.Ho && wo < g.Wo;  // uniform over the L-lane group
     const T* row = omt + (py * TW + px) * g.seg + gl * 3 * K;
     float m[K];
-    float gyv[CPL * E];
-    uint4 gyu[CPL];  // the lane's gy chunks, packed (dot products)
     unsigned outside = 0;
-    // ---- P1: grad_om and bin counts
+    // Sample k of this (pixel, group): halo-local floor corner (yl, xl), fractions, whether
+    // it lies inside the halo, and the in-image corners.  P1 and P3 both call this, so the
+    // contributions P1 counts are exactly the ones P3 files.
+    struct Pt {
+      int yl, xl;
+      float fy, fx;
+      bool fin, in, ok[4];
+    };
+    auto point = [&](int k) {
+      Pt P;
+      const int i = k / 3, j = k % 3;
+      const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
+      float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
+      float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
+      P.fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
+      ty = P.fin ? ty : 0.f;
+      tx = P.fin ? tx : 0.f;
+      const float fly = floorf(ty), flx = floorf(tx);
+      P.fy = ty - fly;
+      P.fx = tx - flx;
+      const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
+      const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
+      P.in = P.fin && (unsigned)yl <= (unsigned)(HH - 2) && (unsigned)xl <= (unsigned)(HWC - 2);
+      P.yl = P.in ? yl : 0;
+      P.xl = P.in ? xl : 0;
+      const int yy = hy0 + P.yl, xx = hx0 + P.xl;
+      const bool vy0 = (unsigned)yy < (unsigned)H, vy1 = (unsigned)(yy + 1) < (unsigned)H;
+      const bool vx0 = (unsigned)xx < (unsigned)W, vx1 = (unsigned)(xx + 1) < (unsigned)W;
+      P.ok[0] = P.in && vy0 && vx0;
+      P.ok[1] = P.in && vy0 && vx1;
+      P.ok[2] = P.in && vy1 && vx0;
+      P.ok[3] = P.in && vy1 && vx1;
+      return P;
+    };
+    // ---- P1: bin counts only (coordinates, no data): shared-memory reductions
     if (active) {
       load_m<T, K>(row, g.softmax, m);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const Pt P = point(k);
+        outside |= (P.fin && !P.in) ? (1u << k) : 0u;
+        const float hy = 1.f - P.fy;
+        const float w[4] = {hy * (1.f - P.fx), hy * P.fx, P.fy * (1.f - P.fx), P.fy * P.fx};
+#pragma unroll
+        for (int r = 0; r < QPL; ++r) {
+          const int q = (lg % 4) + r * L;
+          if (lg < 4 && q < 4 && pick4(P.ok, q) && m[k] * pick4(w, q) != 0.f) {
+            const int tt = (P.yl + (q >> 1)) * HWC + P.xl + (q & 1);
+            atomicAdd(&cnt[gl * NT + tt], 1);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- P2: bin offsets (one in-place exclusive scan over all groups' bins, counts padded
+    // to even; bin i holds entries [offs[i] & ~1, offs[i+1] & ~1)) and fill pointers
+    int* const offs = cnt;
+    {
+      const int total = block_exclusive_scan<true>(offs, GC * NT, wsum);
+      if (tid == 0) offs[GC * NT] = total;
+      for (int i = tid; i < GC * NT; i += blockDim.x) fill[i] = offs[i] & ~1;
+      __syncthreads();
+    }
+    // ---- P3: gathers from the x halo, grad_om partials, and filing of the contributions
+    if (active) {
+      float gyv[CPL * E];
+      uint4 gyu[CPL];  // the lane's gy chunks, packed (dot products)
 #pragma unroll
       for (int h = 0; h < CPL; ++h) {
         uint4 u = *reinterpret_cast<const uint4*>(gyt + (py * TW + px) * GC * DG + gl * DG + co[h]);
@@ -1133,21 +1193,8 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const int i = k / 3, j = k % 3;
-        const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
-        float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
-        float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
-        const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
-        ty = fin ? ty : 0.f;
-        tx = fin ? tx : 0.f;
-        const float fly = floorf(ty), flx = floorf(tx);
-        const float fy = ty - fly, fx = tx - flx;
-        const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
-        const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
-        const bool in = fin && (unsigned)yl <= (unsigned)(HH - 2) && (unsigned)xl <= (unsigned)(HWC - 2);
-        outside |= (fin && !in) ? (1u << k) : 0u;
-        const int ylc = in ? yl : 0, xlc = in ? xl : 0;
-        const uint32_t off = (uint32_t)(ylc * ROWB + xlc * PB);
+        const Pt P = point(k);
+        const uint32_t off = (uint32_t)(P.yl * ROWB + P.xl * PB);
         float S[4];
         float2 S2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
@@ -1160,16 +1207,12 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) S[q] = S2[q].x + S2[q].y;
-        // corner validity (inside the image); halo pixels outside the image hold zeros
-        const int yy = hy0 + ylc, xx = hx0 + xlc;
-        const bool vy0 = (unsigned)yy < (unsigned)H, vy1 = (unsigned)(yy + 1) < (unsigned)H;
-        const bool vx0 = (unsigned)xx < (unsigned)W, vx1 = (unsigned)(xx + 1) < (unsigned)W;
-        const bool ok[4] = {in && vy0 && vx0, in && vy0 && vx1, in && vy1 && vx0, in && vy1 && vx1};
-        const float hy = 1.f - fy, hx = 1.f - fx;
-        const float w[4] = {hy * hx, hy * fx, fy * hx, fy * fx};
+        // halo pixels outside the image hold zeros, so S needs no validity mask
+        const float hy = 1.f - P.fy, hx = 1.f - P.fx;
+        const float w[4] = {hy * hx, hy * P.fx, P.fy * hx, P.fy * P.fx};
         float sgm = w[0] * S[0] + w[1] * S[1] + w[2] * S[2] + w[3] * S[3];
-        float sgy = hx * (S[2] - S[0]) + fx * (S[3] - S[1]);
-        float sgx = hy * (S[1] - S[0]) + fy * (S[3] - S[2]);
+        float sgy = hx * (S[2] - S[0]) + P.fx * (S[3] - S[1]);
+        float sgx = hy * (S[1] - S[0]) + P.fy * (S[3] - S[2]);
 #pragma unroll
         for (int o = 1; o < L; o <<= 1) {
           sgm += __shfl_xor_sync(gmask, sgm, o);
@@ -1178,17 +1221,19 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
         }
         if (lg == 0) {
           float* grow = gomt + item * 3 * K;
-          grow[2 * k] = in ? s * m[k] * sgx : 0.f;
-          grow[2 * k + 1] = in ? s * m[k] * sgy : 0.f;
-          grow[2 * K + k] = in ? sgm : 0.f;
+          grow[2 * k] = P.in ? s * m[k] * sgx : 0.f;
+          grow[2 * k + 1] = P.in ? s * m[k] * sgy : 0.f;
+          grow[2 * K + k] = P.in ? sgm : 0.f;
         }
-        // count this lane's scatter contributions into their halo bins
+        // file this lane's scatter contributions into their bins
 #pragma unroll
         for (int r = 0; r < QPL; ++r) {
           const int q = (lg % 4) + r * L;
-          if (lg < 4 && q < 4 && pick4(ok, q) && m[k] * pick4(w, q) != 0.f) {
-            const int tt = (ylc + (q >> 1)) * HWC + xlc + (q & 1);
-            slots[(k * 4 + q) * SPS + item] = (unsigned short)atomicAdd(&cnt[gl * NT + tt], 1);
+          const float a = m[k] * pick4(w, q);
+          if (lg < 4 && q < 4 && pick4(P.ok, q) && a != 0.f) {
+            const int tt = (P.yl + (q >> 1)) * HWC + P.xl + (q & 1);
+            const int e = atomicAdd(&fill[gl * NT + tt], 1);
+            ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
           }
         }
       }
@@ -1268,48 +1313,8 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       }
     }
     __syncthreads();
-    // ---- P2: bin offsets (one in-place exclusive scan over all groups' bins;
-    // bin i holds entries [offs[i], offs[i+1]))
-    int* const offs = cnt;
-    if (g.dbg & 1) { __syncthreads(); continue; }
-    {
-      const int total = block_exclusive_scan<true>(offs, GC * NT, wsum);
-      if (tid == 0) offs[GC * NT] = total;
-      __syncthreads();
-    }
-    // ---- P3: fill the bins; write the grad_om tile
-    if (active) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        if ((outside >> k) & 1u) continue;
-        const int i = k / 3, j = k % 3;
-        const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
-        float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
-        float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
-        const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
-        if (!fin) continue;
-        const float fly = floorf(ty), flx = floorf(tx);
-        const float fy = ty - fly, fx = tx - flx;
-        const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
-        const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
-        const int yy = hy0 + yl, xx = hx0 + xl;
-        const bool vy0 = (unsigned)yy < (unsigned)H, vy1 = (unsigned)(yy + 1) < (unsigned)H;
-        const bool vx0 = (unsigned)xx < (unsigned)W, vx1 = (unsigned)(xx + 1) < (unsigned)W;
-        const bool ok[4] = {vy0 && vx0, vy0 && vx1, vy1 && vx0, vy1 && vx1};
-        const float hy = 1.f - fy, hx = 1.f - fx;
-        const float w[4] = {hy * hx, hy * fx, fy * hx, fy * fx};
-#pragma unroll
-        for (int r = 0; r < QPL; ++r) {
-          const int q = (lg % 4) + r * L;
-          const float a = m[k] * pick4(w, q);
-          if (lg < 4 && q < 4 && pick4(ok, q) && a != 0.f) {
-            const int tt = (yl + (q >> 1)) * HWC + xl + (q & 1);
-            const int e = (offs[gl * NT + tt] & ~1) + slots[(k * 4 + q) * SPS + item];
-            ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
-          }
-        }
-      }
-    }
+    // ---- grad_om tile write-out (coalesced, warp per pixel); the last group run also
+    // zeroes the padding channels [3GK, S)
     {
       const bool last = g0 + GC == g.G;
       for (int p = tid >> 5; p < npix; p += blockDim.x >> 5) {
@@ -1322,7 +1327,6 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           for (int e = g.G * 3 * K + lane; e < g.S; e += 32) dst[e] = Elem<T>::from_f32(0.f);
       }
     }
-    __syncthreads();
     // ---- P4: pull per (halo pixel, group, PC chunks) and one vector reduction per chunk;
     // PC = 2 chunks per lane amortise the entry loads; the chunk order alternates with
     // the halo pixel so an 8-lane phase still touches 8 distinct bank quads
