@@ -27,18 +27,26 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dcnv4_oracle.c")
 _LIB = os.path.join(_HERE, "libdcnv4_oracle.so")
+_MSRC = os.path.join(_HERE, "msda_oracle.c")
+_MLIB = os.path.join(_HERE, "libmsda_oracle.so")
 _lib = None
+_mlib = None
+
+
+def _gcc(src: str, lib: str, force: bool) -> str:
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+        tmp = lib + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+             "-shared", "-fPIC", "-o", tmp, src, "-lm"])
+        os.replace(tmp, lib)
+    return lib
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (fp64, no fast-math, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
-             "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+    """Compile the oracles with gcc (fp64, no fast-math, no FMA contraction)."""
+    _gcc(_MSRC, _MLIB, force)
+    return _gcc(_SRC, _LIB, force)
 
 
 def _load():
@@ -160,3 +168,83 @@ def abs_scaled_error(gpu, ref, scale) -> float:
     if gpu.size == 0:
         return 0.0
     return float((np.abs(gpu - ref) / den).max())
+
+
+# ---------------------------------------------------------------------------------------
+# Multi-scale deformable attention (R20).  The paper names
+# the operator and says the DCNv4 kernel techniques apply to it; the
+# sampling core is written out in msda_oracle.c.
+
+
+@dataclass(frozen=True)
+class MSDAGeometry:
+    """value [N][S][M][D] over levels `shapes` = ((H_0, W_0), ...), S = sum H_l*W_l;
+    loc [N][Lq][M][L][P][2] (x, y) in [0, 1]; attn [N][Lq][M][L][P]."""
+    N: int
+    Lq: int
+    M: int
+    D: int
+    P: int
+    shapes: tuple
+
+    @property
+    def L(self) -> int:
+        return len(self.shapes)
+
+    @property
+    def S(self) -> int:
+        return sum(h * w for h, w in self.shapes)
+
+    def vec(self) -> np.ndarray:
+        v = [self.N, self.Lq, self.M, self.D, self.L, self.P]
+        for h, w in self.shapes:
+            v += [h, w]
+        return np.array(v, dtype=np.int64)
+
+
+def _mload():
+    global _mlib
+    if _mlib is None:
+        build()
+        lib = ctypes.CDLL(_MLIB)
+        P = ctypes.c_void_p
+        lib.msda_oracle_forward.argtypes = [P] * 6
+        lib.msda_oracle_backward.argtypes = [P] * 11
+        lib.msda_oracle_forward.restype = ctypes.c_int
+        lib.msda_oracle_backward.restype = ctypes.c_int
+        _mlib = lib
+    return _mlib
+
+
+def msda_forward(geom: MSDAGeometry, value, loc, attn, with_abs: bool = False):
+    """out [N][Lq][M][D] in fp64 (msda_oracle.c header).  Returns out or (out, out_abs)."""
+    lib = _mload()
+    g = geom
+    value = _f64(value).reshape(g.N, g.S, g.M, g.D)
+    loc = _f64(loc).reshape(g.N, g.Lq, g.M, g.L, g.P, 2)
+    attn = _f64(attn).reshape(g.N, g.Lq, g.M, g.L, g.P)
+    out = np.empty((g.N, g.Lq, g.M, g.D), np.float64)
+    oa = np.empty_like(out) if with_abs else None
+    gv = g.vec()
+    lib.msda_oracle_forward(_ptr(gv), _ptr(value), _ptr(loc), _ptr(attn), _ptr(out),
+                            _ptr(oa) if with_abs else None)
+    return (out, oa) if with_abs else out
+
+
+def msda_backward(geom: MSDAGeometry, value, loc, attn, gout, with_abs: bool = False):
+    """(grad_value, grad_loc, grad_attn) in fp64; with_abs adds their magnitude scales."""
+    lib = _mload()
+    g = geom
+    value = _f64(value).reshape(g.N, g.S, g.M, g.D)
+    loc = _f64(loc).reshape(g.N, g.Lq, g.M, g.L, g.P, 2)
+    attn = _f64(attn).reshape(g.N, g.Lq, g.M, g.L, g.P)
+    gout = _f64(gout).reshape(g.N, g.Lq, g.M, g.D)
+    gval = np.empty_like(value)
+    gloc = np.empty_like(loc)
+    gattn = np.empty_like(attn)
+    ab = [np.empty_like(a) for a in (gval, gloc, gattn)] if with_abs else [None] * 3
+    gv = g.vec()
+    lib.msda_oracle_backward(_ptr(gv), _ptr(value), _ptr(loc), _ptr(attn), _ptr(gout),
+                             _ptr(gval), _ptr(gloc), _ptr(gattn),
+                             *[(_ptr(a) if a is not None else None) for a in ab])
+    return (gval, gloc, gattn, *ab) if with_abs else (gval, gloc, gattn)

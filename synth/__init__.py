@@ -81,3 +81,37 @@ def make_case(N, H, W, G, D, Ho, Wo, K, S, dtype="f32", images=None, offsets="u2
         gy = torch.stack([image_gy(Ho, Wo, C, n) for n in images]).to(dt) if images else \
             torch.empty((0, Ho, Wo, C), dtype=dt)
     return x, om, gy
+
+
+# ---------------------------------------------------------------------------------------
+# Multi-scale deformable attention inputs (NEXT-3, R20).
+#   value ~ U(-1, 1)                    [N, S, M, D], S = sum_l H_l*W_l
+#   loc   ~ U(-0.1, 1.1) (x, y)         [N, Lq, M, L, P, 2]: normalised sampling points,
+#                                       a margin outside [0, 1] exercises zero padding
+#   attn  ~ U(0, 2/(L*P))               [N, Lq, M, L, P]: positive weights summing to ~1
+#                                       per (query, head), like the caller's softmax
+#   gout  ~ U(-1, 1)                    [N, Lq, M, D]
+TENSOR_VALUE, TENSOR_LOC, TENSOR_ATTN, TENSOR_GOUT = 10, 11, 12, 13
+
+
+def make_msda_case(N, Lq, M, D, P, shapes, dtype="f32", images=None, loc_range=(-0.1, 1.1),
+                   with_gout=True):
+    """CPU tensors (value, loc, attn, gout) for images ``images`` (default range(N))."""
+    images = list(range(N)) if images is None else list(images)
+    L = len(shapes)
+    S = sum(h * w for h, w in shapes)
+    dt = DTYPES[dtype]
+
+    def stack(fn, shape):
+        if not images:
+            return torch.empty((0,) + shape, dtype=dt)
+        return torch.stack([fn(n) for n in images]).to(dt)
+
+    value = stack(lambda n: _uniform((S, M, D), seed_of(TENSOR_VALUE, n), -1.0, 1.0), (S, M, D))
+    loc = stack(lambda n: _uniform((Lq, M, L, P, 2), seed_of(TENSOR_LOC, n), *loc_range),
+                (Lq, M, L, P, 2))
+    attn = stack(lambda n: _uniform((Lq, M, L, P), seed_of(TENSOR_ATTN, n), 0.0, 2.0 / (L * P)),
+                 (Lq, M, L, P))
+    gout = stack(lambda n: _uniform((Lq, M, D), seed_of(TENSOR_GOUT, n), -1.0, 1.0),
+                 (Lq, M, D)) if with_gout else None
+    return value, loc, attn, gout
