@@ -292,21 +292,47 @@ struct Samp {
   float w[4];    // bilinear weights, 0 for out-of-image corners
   bool ok[4];    // corner inside the image
   float fy, fx;  // fractional parts
+  float hy, hx;  // 1 - fractional parts (R11: exact or rounded once)
 };
+
+// Reading R11: the sample offset t = s*(tap + d) (UNIT, s = 1: t = d, the tap is added as an
+// integer by the caller) split into floor, fraction f and complement 1 - f, each with
+// relative error <= 2^-24 even when tiny (an edge sample whose only in-image corner has
+// weight ~f must not lose it).  UNIT: d - floor(d) and (floor(d) + 1) - d are exact
+// (Sterbenz).  Otherwise s*(tap + d) is formed exactly in fp64 (24 x 26 significant bits)
+// and f, 1 - f are rounded once from it.  |t| > 2^20 or NaN: fin = false (sample dropped).
+template <bool UNIT>
+__device__ __forceinline__ void split_t(float s, int tap, float d, bool& fin, int& fl, float& f,
+                                        float& f1) {
+  if constexpr (UNIT) {
+    fin = fabsf(d) <= 1048576.f;
+    const float t = fin ? d : 0.f;
+    const float flf = floorf(t);
+    fl = (int)flf;
+    f = t - flf;
+    f1 = (flf + 1.f) - t;
+  } else {
+    const double t = (double)s * ((double)tap + (double)d);
+    fin = fabs(t) <= 1048576.0;
+    const double tt = fin ? t : 0.0;
+    const double fld = floor(tt);
+    fl = (int)fld;
+    f = (float)(tt - fld);
+    f1 = (float)((fld + 1.0) - tt);
+  }
+}
 
 template <bool UNIT>
 __device__ __forceinline__ void sample(int H, int W, unsigned C, float s, int yb, int xb, int tapy,
                                        int tapx, float dx, float dy, unsigned gbase, Samp& c) {
-  float ty = UNIT ? dy : s * ((float)tapy + dy);
-  float tx = UNIT ? dx : s * ((float)tapx + dx);
-  const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;  // false for NaN
-  ty = fin ? ty : 0.f;
-  tx = fin ? tx : 0.f;
-  const float fly = floorf(ty), flx = floorf(tx);
-  c.fy = ty - fly;
-  c.fx = tx - flx;
-  const int y0 = yb + (UNIT ? tapy : 0) + (int)fly;
-  const int x0 = xb + (UNIT ? tapx : 0) + (int)flx;
+  bool finy, finx;
+  int fly, flx;
+  float hy, hx;
+  split_t<UNIT>(s, tapy, dy, finy, fly, c.fy, hy);
+  split_t<UNIT>(s, tapx, dx, finx, flx, c.fx, hx);
+  const bool fin = finy && finx;
+  const int y0 = yb + (UNIT ? tapy : 0) + fly;
+  const int x0 = xb + (UNIT ? tapx : 0) + flx;
   const bool vy0 = fin && (unsigned)y0 < (unsigned)H, vy1 = fin && (unsigned)(y0 + 1) < (unsigned)H;
   const bool vx0 = (unsigned)x0 < (unsigned)W, vx1 = (unsigned)(x0 + 1) < (unsigned)W;
   const int y0c = min(max(y0, 0), H - 1), y1c = min(max(y0 + 1, 0), H - 1);
@@ -317,7 +343,8 @@ __device__ __forceinline__ void sample(int H, int W, unsigned C, float s, int yb
   c.o[2] = (r1 + x0c) * C + gbase;
   c.o[3] = (r1 + x1c) * C + gbase;
   c.ok[0] = vy0 && vx0; c.ok[1] = vy0 && vx1; c.ok[2] = vy1 && vx0; c.ok[3] = vy1 && vx1;
-  const float hy = 1.f - c.fy, hx = 1.f - c.fx;
+  c.hy = hy;
+  c.hx = hx;
   c.w[0] = c.ok[0] ? hy * hx : 0.f;
   c.w[1] = c.ok[1] ? hy * c.fx : 0.f;
   c.w[2] = c.ok[2] ? c.fy * hx : 0.f;
@@ -582,7 +609,7 @@ DCNV4_DOT_HALF(__nv_bfloat16, "bf16")
 #undef DCNV4_DOT_HALF
 
 template <typename T, int NCH, int CPL, bool UNIT>
-__global__ void __launch_bounds__(256) fwd33_kernel(const __grid_constant__ CUtensorMap xmap, Geo g,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 0 : 2) fwd33_kernel(const __grid_constant__ CUtensorMap xmap, Geo g,
                                                     const T* __restrict__ x,
                                                     const T* __restrict__ om,
                                                     T* __restrict__ y) {
@@ -693,16 +720,15 @@ __global__ void __launch_bounds__(256) fwd33_kernel(const __grid_constant__ CUte
       auto fetch = [&](int k, Fetched& F) {
         const int i = k / 3, j = k % 3;
         const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
-        float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
-        float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
-        const bool fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
-        ty = fin ? ty : 0.f;
-        tx = fin ? tx : 0.f;
-        const float fly = floorf(ty), flx = floorf(tx);
-        const float fy = ty - fly, fx = tx - flx;
+        bool finy, finx;
+        int fly, flx;
+        float fy, fx, hy, hx;
+        split_t<UNIT>(s, j - 1, dy, finy, fly, fy, hy);
+        split_t<UNIT>(s, i - 1, dx, finx, flx, fx, hx);
+        const bool fin = finy && finx;
         // local halo coordinates: halo origin = (h0 - ph - 2, w0 - pw - 2)
-        const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
-        const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
+        const int yl = py + (UNIT ? j + 2 : 3) + fly;
+        const int xl = px + (UNIT ? i + 2 : 3) + flx;
         const bool in = (unsigned)yl <= (unsigned)(HH - 2) && (unsigned)xl <= (unsigned)(HWC - 2);
         outside |= (fin && !in) ? (1u << k) : 0u;
         const float mk = (fin && in) ? m[k] : 0.f;
@@ -715,8 +741,8 @@ __global__ void __launch_bounds__(256) fwd33_kernel(const __grid_constant__ CUte
           F.u[2][h] = lds16(a0 + ROWB);
           F.u[3][h] = lds16(a0 + ROWB + PB);
         }
-        const float my = mk * (1.f - fy), ny = mk * fy;
-        F.a[0] = my * (1.f - fx); F.a[1] = my * fx; F.a[2] = ny * (1.f - fx); F.a[3] = ny * fx;
+        const float my = mk * hy, ny = mk * fy;
+        F.a[0] = my * hx; F.a[1] = my * fx; F.a[2] = ny * hx; F.a[3] = ny * fx;
       };
       auto accum = [&](const Fetched& F) {
 #pragma unroll
@@ -884,7 +910,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x
           }
         }
       }
-      const float hy = 1.f - c.fy, hx = 1.f - c.fx;
+      const float hy = c.hy, hx = c.hx;
       float sgm = c.w[0] * S[0] + c.w[1] * S[1] + c.w[2] * S[2] + c.w[3] * S[3];
       float sgy = hx * (S[2] - S[0]) + c.fx * (S[3] - S[1]);
       float sgx = hy * (S[1] - S[0]) + c.fy * (S[3] - S[2]);
@@ -1123,23 +1149,20 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
     // contributions P1 counts are exactly the ones P3 files.
     struct Pt {
       int yl, xl;
-      float fy, fx;
+      float fy, fx, hy, hx;  // fractions and 1 - fractions (R11)
       bool fin, in, ok[4];
     };
     auto point = [&](int k) {
       Pt P;
       const int i = k / 3, j = k % 3;
       const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
-      float ty = UNIT ? dy : s * ((float)(j - 1) + dy);
-      float tx = UNIT ? dx : s * ((float)(i - 1) + dx);
-      P.fin = fabsf(ty) <= 1048576.f && fabsf(tx) <= 1048576.f;
-      ty = P.fin ? ty : 0.f;
-      tx = P.fin ? tx : 0.f;
-      const float fly = floorf(ty), flx = floorf(tx);
-      P.fy = ty - fly;
-      P.fx = tx - flx;
-      const int yl = py + (UNIT ? j + 2 : 3) + (int)fly;
-      const int xl = px + (UNIT ? i + 2 : 3) + (int)flx;
+      bool finy, finx;
+      int fly, flx;
+      split_t<UNIT>(s, j - 1, dy, finy, fly, P.fy, P.hy);
+      split_t<UNIT>(s, i - 1, dx, finx, flx, P.fx, P.hx);
+      P.fin = finy && finx;
+      const int yl = py + (UNIT ? j + 2 : 3) + fly;
+      const int xl = px + (UNIT ? i + 2 : 3) + flx;
       P.in = P.fin && (unsigned)yl <= (unsigned)(HH - 2) && (unsigned)xl <= (unsigned)(HWC - 2);
       P.yl = P.in ? yl : 0;
       P.xl = P.in ? xl : 0;
@@ -1159,8 +1182,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       for (int k = 0; k < K; ++k) {
         const Pt P = point(k);
         outside |= (P.fin && !P.in) ? (1u << k) : 0u;
-        const float hy = 1.f - P.fy;
-        const float w[4] = {hy * (1.f - P.fx), hy * P.fx, P.fy * (1.f - P.fx), P.fy * P.fx};
+        const float w[4] = {P.hy * P.hx, P.hy * P.fx, P.fy * P.hx, P.fy * P.fx};
 #pragma unroll
         for (int r = 0; r < QPL; ++r) {
           const int q = (lg % 4) + r * L;
@@ -1208,7 +1230,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
 #pragma unroll
         for (int q = 0; q < 4; ++q) S[q] = S2[q].x + S2[q].y;
         // halo pixels outside the image hold zeros, so S needs no validity mask
-        const float hy = 1.f - P.fy, hx = 1.f - P.fx;
+        const float hy = P.hy, hx = P.hx;
         const float w[4] = {hy * hx, hy * P.fx, P.fy * hx, P.fy * P.fx};
         float sgm = w[0] * S[0] + w[1] * S[1] + w[2] * S[2] + w[3] * S[3];
         float sgy = hx * (S[2] - S[0]) + P.fx * (S[3] - S[1]);
@@ -1285,7 +1307,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
               }
             }
           }
-          const float hy = 1.f - c.fy, hx = 1.f - c.fx;
+          const float hy = c.hy, hx = c.hx;
           float sgm = c.w[0] * S[0] + c.w[1] * S[1] + c.w[2] * S[2] + c.w[3] * S[3];
           float sgy = hx * (S[2] - S[0]) + c.fx * (S[3] - S[1]);
           float sgx = hy * (S[1] - S[0]) + c.fy * (S[3] - S[2]);

@@ -87,7 +87,10 @@ def run_case(g: oracle.Geometry, dtype="f32", offsets="u2", images=None, backwar
         gx, gom = pkg.backward(xd, omd, gyd, deterministic=deterministic, **kw)
     torch.cuda.synchronize()
     sel = list(range(g.N)) if check_images is None else list(check_images)
-    gs = oracle.Geometry(**{**g.__dict__, "N": len(sel)})
+    # the oracle sees exactly what the GPU sees: quantised inputs and the
+    # fp32 offset_scale of dcnv4_params (e.g. 1.3f, not the fp64 1.3)
+    gs = oracle.Geometry(**{**g.__dict__, "N": len(sel),
+                            "offset_scale": float(np.float32(g.offset_scale))})
     xs, oms, gys = x[sel], om[sel], gy[sel]
     y_ref, y_abs = oracle.forward(gs, xs, oms, with_abs=True)
     qf = QFLOOR[dtype]
@@ -122,6 +125,8 @@ CASES = [
     ("k2x2_even", _geom(1, 9, 8, 2, 16, k=(2, 2), p=(0, 1)), "u2"),
     ("scale0.5", _geom(2, 11, 10, 2, 16, scale=0.5), "u2"),
     ("scale2", _geom(2, 11, 10, 2, 16, scale=2.0), "u2"),
+    ("scale0.7", _geom(2, 11, 10, 2, 16, scale=0.7), "u2"),
+    ("halo_G4_scale1.3", _geom(2, 12, 10, 4, 16, scale=1.3), "u2"),
     ("om_stride_pad", _geom(2, 9, 10, 3, 16, S=3 * 3 * 9 + 5), "u2"),
     ("om_stride_pad8", _geom(2, 9, 10, 2, 16, S=56), "u2"),
     ("zero_offsets_kinks", _geom(2, 10, 10, 2, 16), "zero"),
