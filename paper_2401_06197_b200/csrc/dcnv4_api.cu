@@ -542,6 +542,9 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 }  // namespace
 
+// shared with msda.cu: one thread-local message for every entry point of the library
+void dcnv4_internal_set_error(const char* msg) { snprintf(g_err, sizeof(g_err), "%s", msg); }
+
 extern "C" {
 
 int dcnv4_version(void) { return DCNV4_VERSION; }

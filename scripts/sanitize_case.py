@@ -29,6 +29,8 @@ for (N, H, W, G, D, dt, k, st, pd, dl, sc, off, sm) in cases:
     kw = dict(group=G, kernel_size=k, stride=st, pad=pd, dilation=dl, offset_scale=sc, softmax=sm)
     y = pkg.forward(x, om, **kw)
     gx, gom = pkg.backward(x, om, gy, **kw)
+    gxd, _ = pkg.backward(x, om, gy, deterministic=True, **kw)  # int64 fixed-point path
     torch.cuda.synchronize()
     print("ok", (N, H, W, G, D, dt, k, st, pd, dl, sc, off, sm), float(y.float().abs().sum()),
-          float(gx.float().abs().sum()), float(gom.float().abs().sum()))
+          float(gx.float().abs().sum()), float(gom.float().abs().sum()),
+          float(gxd.float().abs().sum()))

@@ -5,6 +5,7 @@ import os
 import re
 
 import pytest
+import torch
 
 import oracle
 import paper_2401_06197_b200 as pkg
@@ -14,15 +15,44 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "dcnv4.h")
 
 
+MSDA_HEADER = os.path.join(ROOT, "include", "msda.h")
+
+
 def _declared():
-    src = open(HEADER).read()
-    return re.findall(r"DCNV4_API\s+[\w\s\*]+?\b(dcnv4_\w+)\s*\(", src)
+    out = []
+    for h in (HEADER, MSDA_HEADER):
+        src = open(h).read()
+        out += re.findall(r"DCNV4_API\s+[\w\s\*]+?\b((?:dcnv4|msda)_\w+)\s*\(", src)
+    return out
 
 
 def test_header_declares_the_boundary():
     names = set(_declared())
     assert {"dcnv4_forward", "dcnv4_backward", "dcnv4_output_size", "dcnv4_last_error",
             "dcnv4_version", "dcnv4_backward_workspace_bytes", "dcnv4_launch_info"} <= names
+    assert {"msda_forward", "msda_backward", "msda_value_tokens",
+            "msda_backward_workspace_bytes"} <= names
+
+
+def test_msda_params_and_validation():
+    from paper_2401_06197_b200 import msda
+    assert ctypes.sizeof(msda.MSDAParams) == 96
+    p = msda.make_params(2, 100, 8, 32, 4, [(10, 12), (5, 6), (3, 3), (2, 2)])
+    assert msda.value_tokens(p) == 120 + 30 + 9 + 4
+    assert msda.workspace_bytes(p, torch.float32) == 0
+    assert msda.workspace_bytes(p, torch.bfloat16) == 2 * 163 * 8 * 32 * 4
+    lib = pkg.lib()
+    bad = msda.make_params(1, 4, 2, 6, 1, [(3, 3)])  # D*4 = 24 B
+    assert lib.msda_forward(ctypes.byref(bad), 0, None, None, None, None, None) == b.ERR_UNSUPPORTED
+    assert b"16" in lib.dcnv4_last_error()
+    bad = msda.make_params(1, 4, 2, 8, 1, [(3, 0)])
+    assert lib.msda_forward(ctypes.byref(bad), 0, None, None, None, None, None) == b.ERR_INVALID_ARG
+    assert b"level 0" in lib.dcnv4_last_error()
+    bad = msda.make_params(1, 4, 2, 8, 0, [(3, 3)])
+    assert lib.msda_forward(ctypes.byref(bad), 0, None, None, None, None, None) == b.ERR_INVALID_ARG
+    assert b"P" in lib.dcnv4_last_error()
+    ok = msda.make_params(0, 4, 2, 8, 1, [(3, 3)])  # empty batch: no-op, no CUDA call
+    assert lib.msda_forward(ctypes.byref(ok), 0, None, None, None, None, None) == b.OK
 
 
 def test_library_exports_every_declared_symbol():
