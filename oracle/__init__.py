@@ -248,3 +248,68 @@ def msda_backward(geom: MSDAGeometry, value, loc, attn, gout, with_abs: bool = F
                              _ptr(gval), _ptr(gloc), _ptr(gattn),
                              *[(_ptr(a) if a is not None else None) for a in ab])
     return (gval, gloc, gattn, *ab) if with_abs else (gval, gloc, gattn)
+
+
+# ---------------------------------------------------------------------------------------
+# DCNv4 module path (R21).  P:334: "the linear layers for
+# computing offset and dynamic weights can actually be combined into one linear layer",
+# and the depthwise conv in front of it "can also be removed" (latency-first variant);
+# the "lightweight" module has no input/output projections, so the value
+# the operator samples is the module input itself.  Reading R21: the linear's output is
+# stored in the storage dtype T before the operator reads it (what an unfused module
+# holds between its two layers), so the oracle rounds it once, fp64 -> T, RN-even.
+
+_ROUND = {"f32": (24, -125, 3.4028234663852886e38), "f16": (11, -13, 65504.0),
+          "bf16": (8, -125, 3.3895313892515355e38)}
+
+
+def round_to(v, dtype: str) -> np.ndarray:
+    """Round fp64 values to the nearest `dtype` value (ties to even), subnormals and
+    overflow to +-inf included.  v = m * 2^e with m in [0.5, 1): the quantum is
+    2^(max(e, emin) - p) for p significant bits; np.rint rounds half to even."""
+    p, emin, vmax = _ROUND[dtype]
+    v = np.asarray(v, dtype=np.float64)
+    _, e = np.frexp(v)
+    q = np.ldexp(1.0, np.maximum(e, emin) - p)
+    r = np.rint(v / q) * q
+    # |v| at or beyond the rounding midpoint above the largest finite value -> inf
+    big = np.abs(v) >= vmax + np.ldexp(1.0, np.frexp(vmax)[1] - p - 1)
+    return np.where(big, np.copysign(np.inf, v), r)
+
+
+def offset_mask_linear(feat, weight, bias, S: int, dtype: str = "f32", with_abs: bool = False):
+    """om[r, j] = round_T(sum_c feat[r, c] * weight[j, c] + bias[j]) for j < J = weight
+    rows (= 3GK), om[r, j] = 0 for J <= j < S (reading R21).
+
+    feat [R, C_in], weight [J, C_in], bias [J] (or None).  The contraction is one fp64
+    matrix product (a library primitive standing for the linear layer's definition).
+    Returns om (fp64 holding T values) or, with_abs, (om, om_exact, om_abs) where
+    om_exact is the unrounded fp64 result and om_abs = |feat| @ |weight|^T + |bias|."""
+    f = _f64(feat)
+    w = _f64(weight)
+    R, J = f.shape[0], w.shape[0]
+    b = np.zeros(J) if bias is None else _f64(bias).reshape(J)
+    exact = np.zeros((R, S))
+    exact[:, :J] = f @ w.T + b
+    om = round_to(exact, dtype)
+    if not with_abs:
+        return om
+    ab = np.zeros((R, S))
+    ab[:, :J] = np.abs(f) @ np.abs(w).T + np.abs(b)
+    return om, exact, ab
+
+
+def module_forward(geom: Geometry, x, weight, bias, dtype: str = "f32", with_abs: bool = False):
+    """Lightweight DCNv4 module forward: om = offset_mask_linear(x)
+    at every output pixel (stride 1, 'same' output, so the linear reads x[n, ho, wo]),
+    then y = DCNv4(x, om) (Eq. (1)-(2)).  Returns y, or (y, y_abs, om)."""
+    Ho, Wo = geom.out_hw()
+    if (Ho, Wo) != (geom.H, geom.W):
+        raise ValueError("module_forward needs Ho == H and Wo == W (the linear reads x per pixel)")
+    xf = _f64(x).reshape(geom.N * geom.H * geom.W, geom.C)
+    om = offset_mask_linear(xf, weight, bias, geom.S, dtype)
+    om = om.reshape(geom.N, Ho, Wo, geom.S)
+    if not with_abs:
+        return forward(geom, xf, om)
+    y, ya = forward(geom, xf, om, with_abs=True)
+    return y, ya, om

@@ -29,9 +29,12 @@ METRICS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
+    if rep.endswith(".csv"):  # an already exported `ncu -i rep --page raw --csv`
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
+    rows = [r for r in csv.reader(io.StringIO(out)) if r and not r[0].startswith("==")]
     hdr, units = rows[0], rows[1]
     res = []
     for vals in rows[2:]:
