@@ -1,0 +1,64 @@
+/*
+ * dcnv4_module.h -- C ABI of the DCNv4 module path in libdcnv4.so.
+ *
+ * The operation.  PAPER.md P:334 ("Micro design in DCN module"): "the linear layers for
+ * computing offset and dynamic weights can actually be combined into one linear layer",
+ * and the depthwise conv in front of it "can also be removed with only a minor
+ * performance sacrifice" when latency comes first.  P:1003-1009: the "lightweight"
+ * DCNv4 module has no input/output projections, i.e. the operator samples the module
+ * input itself.  So the module's offset/mask branch is one linear layer
+ *
+ *     om[r][j] = sum_{c < C_in} feat[r][c] * weight[j][c] + bias[j],   j < J = 3*G*K,
+ *
+ * over every output pixel r = (n, ho, wo), producing the fused offset_mask that
+ * include/dcnv4.h's dcnv4_forward reads (layout there: per group
+ * [dx_0, dy_0, ..., dx_{K-1}, dy_{K-1}, m_0, ..., m_{K-1}]).
+ *
+ * Reading R21: the linear's result is rounded once to the storage dtype T
+ * (round-to-nearest-even) before the operator reads it -- exactly what an unfused module
+ * stores between its two layers -- so dcnv4_module_forward and the two-call path
+ * (dcnv4_offset_mask_linear + dcnv4_forward) compute the same function.
+ *
+ * Arithmetic: the contraction runs on the sm_100a 5th-generation tensor cores
+ * (tcgen05.mma kind::f16, operands staged in shared memory by TMA, fp32 accumulators in
+ * tensor memory); the bias is added in fp32 and the sum rounded to T.  Only DCNV4_F16
+ * and DCNV4_BF16 are supported (DCNV4_F32 returns DCNV4_ERR_UNSUPPORTED: fp32 operands
+ * would need the tf32 kind, which does not meet the fp32 parity bar).
+ *
+ * Conventions shared with dcnv4.h: the caller owns every buffer and the stream; the
+ * library never allocates, frees, synchronises or changes the device; pointers are
+ * device pointers on the current device; calls are asynchronous on `stream` and
+ * capturable into CUDA graphs; errors are returned as dcnv4_status with
+ * dcnv4_last_error() naming the argument, never printed or thrown.
+ */
+#ifndef DCNV4_MODULE_H_
+#define DCNV4_MODULE_H_
+
+#include "dcnv4.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Fused offset/mask linear layer on tcgen05 tensor cores.
+ *   p        geometry; rows R = N*Ho*Wo (Ho, Wo from dcnv4_output_size), J = 3*G*K,
+ *            S = p->om_stride (0 => J).
+ *   feat     [R][C_in]  T, row-major (for the lightweight module at stride 1 with
+ *            "same" padding this is x itself: feat[(n*H + h)*W + w][c] = x[n][h][w][c]).
+ *   weight   [J][C_in]  T, row-major (nn.Linear layout: out_features x in_features).
+ *   bias     [J]        T, or NULL for no bias.
+ *   offset_mask [R][S]  T, fully overwritten: om[r][j] = RN_T(sum_c feat*weight + bias)
+ *            for j < J, 0 for J <= j < S.
+ * Requirements: dtype F16 or BF16 (else UNSUPPORTED); C_in >= 8 and C_in % 8 == 0,
+ * S % 8 == 0 (16-B row pitches; else UNSUPPORTED); feat, weight, offset_mask 16-B
+ * aligned, bias 2-B aligned (else MISALIGNED); R < 2^31 (else SHAPE).  N = 0: no-op.
+ * One kernel launch (persistent grid, one CTA per SM).  Bit-deterministic.            */
+DCNV4_API int dcnv4_offset_mask_linear(const dcnv4_params *p, dcnv4_dtype dtype, int32_t C_in,
+                                       const void *feat, const void *weight, const void *bias,
+                                       void *offset_mask, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DCNV4_MODULE_H_ */

@@ -115,3 +115,25 @@ def make_msda_case(N, Lq, M, D, P, shapes, dtype="f32", images=None, loc_range=(
     gout = stack(lambda n: _uniform((Lq, M, D), seed_of(TENSOR_GOUT, n), -1.0, 1.0),
                  (Lq, M, D)) if with_gout else None
     return value, loc, attn, gout
+
+
+# ---------------------------------------------------------------------------------------
+# Module-path inputs (NEXT-2, R21): the fused offset/mask
+# linear layer's parameters, drawn like a trained layer's scale so that its
+# outputs land in the operator's working ranges for x ~ U(-1, 1):
+#   weight [J, C], J = 3*G*K: offset rows ~ U(-1, 1) * 2*sqrt(3/C) (offsets of std
+#   ~1.15 px), mask rows ~ U(-1, 1) * sqrt(3/C) (std ~0.58);  bias ~ U(-0.5, 0.5).
+TENSOR_WEIGHT, TENSOR_BIAS = 20, 21
+
+
+def make_linear(C, G, K, dtype="f32", seed=0):
+    """CPU tensors (weight [3GK, C], bias [3GK]) in ``dtype``."""
+    J = 3 * G * K
+    g = torch.Generator().manual_seed(seed_of(TENSOR_WEIGHT, seed))
+    w = (torch.rand((J, C), generator=g, dtype=torch.float32) * 2.0 - 1.0) * (3.0 / C) ** 0.5
+    scale = torch.ones(G, 3 * K)
+    scale[:, : 2 * K] = 2.0
+    w = w * scale.reshape(J, 1)
+    g = torch.Generator().manual_seed(seed_of(TENSOR_BIAS, seed))
+    b = torch.rand((J,), generator=g, dtype=torch.float32) - 0.5
+    return w.to(DTYPES[dtype]), b.to(DTYPES[dtype])

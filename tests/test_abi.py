@@ -16,11 +16,12 @@ HEADER = os.path.join(ROOT, "include", "dcnv4.h")
 
 
 MSDA_HEADER = os.path.join(ROOT, "include", "msda.h")
+MODULE_HEADER = os.path.join(ROOT, "include", "dcnv4_module.h")
 
 
 def _declared():
     out = []
-    for h in (HEADER, MSDA_HEADER):
+    for h in (HEADER, MSDA_HEADER, MODULE_HEADER):
         src = open(h).read()
         out += re.findall(r"DCNV4_API\s+[\w\s\*]+?\b((?:dcnv4|msda)_\w+)\s*\(", src)
     return out
@@ -32,6 +33,29 @@ def test_header_declares_the_boundary():
             "dcnv4_version", "dcnv4_backward_workspace_bytes", "dcnv4_launch_info"} <= names
     assert {"msda_forward", "msda_backward", "msda_value_tokens",
             "msda_backward_workspace_bytes"} <= names
+    assert "dcnv4_offset_mask_linear" in names
+
+
+def test_offset_mask_linear_validation():
+    """Host-side checks of dcnv4_offset_mask_linear return before any CUDA call."""
+    from paper_2401_06197_b200 import module
+    lib = module._lib()
+    p = b.make_params(1, 8, 8, 4, 16, 3, 1, 1, 1, 1.0, 112)
+    args = (64, None, None, None, None, None)
+    assert lib.dcnv4_offset_mask_linear(ctypes.byref(p), 0, *args) == b.ERR_UNSUPPORTED
+    assert b"F32" in lib.dcnv4_last_error()
+    assert lib.dcnv4_offset_mask_linear(ctypes.byref(p), 1, 60, *args[1:]) == b.ERR_UNSUPPORTED
+    assert b"C_in" in lib.dcnv4_last_error()
+    p2 = b.make_params(1, 8, 8, 4, 16, 3, 1, 1, 1, 1.0, 108)  # 108 % 8 != 0
+    assert lib.dcnv4_offset_mask_linear(ctypes.byref(p2), 1, *args) == b.ERR_UNSUPPORTED
+    assert b"om_stride" in lib.dcnv4_last_error()
+    p3 = b.make_params(1, 8, 8, 4, 16, 3, 1, 1, 1, 1.0, 104)  # < 3GK
+    assert lib.dcnv4_offset_mask_linear(ctypes.byref(p3), 1, *args) == b.ERR_SHAPE
+    assert lib.dcnv4_offset_mask_linear(ctypes.byref(p), 1, *args) == b.ERR_INVALID_ARG
+    assert b"feat" in lib.dcnv4_last_error()
+    p0 = b.make_params(0, 8, 8, 4, 16, 3, 1, 1, 1, 1.0, 112)  # empty batch: no-op
+    assert lib.dcnv4_offset_mask_linear(ctypes.byref(p0), 2, *args) == b.OK
+    assert module.om_stride_for(4) == 112 and module.om_stride_for(32) == 864
 
 
 def test_msda_params_and_validation():
