@@ -57,6 +57,25 @@ DCNV4_API int dcnv4_offset_mask_linear(const dcnv4_params *p, dcnv4_dtype dtype,
                                        const void *feat, const void *weight, const void *bias,
                                        void *offset_mask, void *stream);
 
+/* Fused lightweight-module forward (P:334 + P:1003-1009), one kernel launch:
+ *   y = DCNv4(x, RN_T(x . weight^T + bias))     (Eq. (1)-(2) with the om of R21)
+ * The offset_mask of each 16 x 8-pixel tile is computed on the tensor cores (tcgen05,
+ * fp32 accumulation in TMEM), rounded to T, and consumed from shared memory by the
+ * aggregation in the same CTA: it is never written to memory.  The result equals
+ * dcnv4_offset_mask_linear followed by dcnv4_forward (same rounding of om, same
+ * aggregation arithmetic) up to the fp32 summation order of the linear.
+ *   p        geometry: kernel 3x3, stride 1, pad 1, dilation 1 (else UNSUPPORTED);
+ *            p->om_stride and p->deterministic are ignored; p->softmax and
+ *            p->offset_scale apply as in dcnv4_forward.
+ *   input    x [N][H][W][G*D] T;  weight [3GK][G*D] T;  bias [3GK] T or NULL;
+ *   output   y [N][H][W][G*D] T, fully overwritten (must not alias input).
+ * Requirements: dtype F16/BF16 (F32 -> UNSUPPORTED); D*sizeof(T) in {32, 64, 128} B and
+ * G a multiple of 128 / (D*sizeof(T)) (UNSUPPORTED otherwise); input, weight, output
+ * 16-B aligned, bias 2-B aligned (MISALIGNED).  Bit-deterministic.  N = 0: no-op.     */
+DCNV4_API int dcnv4_module_forward(const dcnv4_params *p, dcnv4_dtype dtype, const void *input,
+                                   const void *weight, const void *bias, void *output,
+                                   void *stream);
+
 #ifdef __cplusplus
 }
 #endif

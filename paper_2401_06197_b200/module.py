@@ -30,6 +30,8 @@ def _lib():
         L.dcnv4_offset_mask_linear.argtypes = [ctypes.POINTER(Params), ctypes.c_int, ctypes.c_int32,
                                                VP, VP, VP, VP, VP]
         L.dcnv4_offset_mask_linear.restype = ctypes.c_int
+        L.dcnv4_module_forward.argtypes = [ctypes.POINTER(Params), ctypes.c_int, VP, VP, VP, VP, VP]
+        L.dcnv4_module_forward.restype = ctypes.c_int
         _bound = True
     return L
 
@@ -70,3 +72,22 @@ def module_forward(x: torch.Tensor, weight: torch.Tensor, bias: Optional[torch.T
     tensor cores, then y = DCNv4(x, om).  Returns y."""
     om = offset_mask_linear(x, weight, bias, group, om_stride, out=om_out)
     return dcnv4_forward(x, om, group, 3, 1, 1, 1, offset_scale, out=out)
+
+
+def forward_fused(x: torch.Tensor, weight: torch.Tensor, bias: Optional[torch.Tensor], group: int,
+                  offset_scale=1.0, softmax=False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Fused lightweight DCNv4 module forward (3x3, stride 1, pad 1), ONE kernel
+    (dcnv4_module_forward): each 16x8-pixel tile's offset_mask is computed on the tensor
+    cores and consumed from shared memory, never written to memory."""
+    ts = [x, weight] + ([bias] if bias is not None else [])
+    _check_tensors(*ts)
+    N, H, W, C = x.shape
+    if C % group:
+        raise ValueError(f"C = {C} is not divisible by group = {group}")
+    p = make_params(N, H, W, group, C // group, 3, 1, 1, 1, offset_scale, 0, softmax)
+    if out is None:
+        out = torch.empty_like(x)
+    with torch.cuda.device(x.device):
+        _check(_lib().dcnv4_module_forward(ctypes.byref(p), DTYPE_CODE[x.dtype], _ptr(x), _ptr(weight),
+                                           _ptr(bias), _ptr(out), ctypes.c_void_p(_stream_ptr(x))))
+    return out

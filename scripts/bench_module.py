@@ -54,14 +54,17 @@ def main():
         xd, wd, bd = x.to(dev), w.to(dev), b.to(dev)
         om = torch.empty((N, H, W, S), dtype=xd.dtype, device=dev)
         y = torch.empty_like(xd)
+        y2 = torch.empty_like(xd)
         calls = [("linear", lambda: module.offset_mask_linear(xd, wd, bd, G, S, out=om)),
-                 ("dcnv4_fwd", lambda: binding.forward(xd, om, G, out=y))]
+                 ("dcnv4_fwd", lambda: binding.forward(xd, om, G, out=y)),
+                 ("fused", lambda: module.forward_fused(xd, wd, bd, G, out=y2))]
         with torch.cuda.stream(stream):
             for _ in range(3):
                 for _, fn in calls:
                     fn()
         stream.synchronize()
-        evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 * args.reps + 1)]
+        nc = len(calls)
+        evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(nc * args.reps + 1)]
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             evs[0].record(stream)
@@ -74,8 +77,10 @@ def main():
         with torch.cuda.stream(stream):
             graph.replay()
         torch.cuda.synchronize()
-        lin = sorted(evs[2 * r].elapsed_time(evs[2 * r + 1]) for r in range(args.reps))[args.reps // 2]
-        dcn = sorted(evs[2 * r + 1].elapsed_time(evs[2 * r + 2]) for r in range(args.reps))[args.reps // 2]
+        med = [sorted(evs[nc * r + c].elapsed_time(evs[nc * r + c + 1]) for r in range(args.reps))[args.reps // 2]
+               for c in range(nc)]
+        lin, dcn, fus = med
+        same = torch.mean((y == y2).double()).item()
         R, J = N * H * W, 3 * G * K
         by = (R * C + J * C + R * S) * 2
         fl = 2.0 * R * C * J
@@ -83,11 +88,14 @@ def main():
                      "linear_us": round(lin * 1e3, 2), "linear_alg_bytes": by,
                      "linear_GBs": round(by / lin / 1e6, 1), "linear_frac_hbm": round(by / lin / 1e6 / peak_bw, 4),
                      "linear_TFLOPs": round(fl / lin / 1e9, 1), "linear_frac_tc": round(fl / lin / 1e9 / peak_tf, 4),
-                     "dcnv4_fwd_us": round(dcn * 1e3, 2), "module_us": round((lin + dcn) * 1e3, 2)})
+                     "dcnv4_fwd_us": round(dcn * 1e3, 2), "module_us": round((lin + dcn) * 1e3, 2),
+                     "fused_us": round(fus * 1e3, 2), "fused_vs_two_call_bit_equal": round(same, 5)})
         del graph
-    tot = sum(r["module_us"] for r in rows)
-    line = {"metric": "DCNv4 lightweight module forward (fused offset/mask linear on tcgen05 + DCNv4)",
-            "value": round(N / (tot * 1e-6), 2), "unit": "imgs/s", "n_gpus": 1, "dtype": args.dtype,
+    tot = sum(r["fused_us"] for r in rows)
+    tot2 = sum(r["module_us"] for r in rows)
+    line = {"metric": "DCNv4 lightweight module forward: fused kernel (value) vs linear + dcnv4_forward (two_call)",
+            "value": round(N / (tot * 1e-6), 2), "unit": "imgs/s",
+            "two_call_imgs_s": round(N / (tot2 * 1e-6), 2), "n_gpus": 1, "dtype": args.dtype,
             "data": "synthetic", "config": {"workload": f"module_{args.workload}", "batch": N, "reps": args.reps,
                                             "l2": "per-stage working sets up to 0.2 GB; no flush"},
             "peaks": {"hbm_gbs": peak_bw, "tc_tflops": peak_tf, "source": src}, "stages": rows}
