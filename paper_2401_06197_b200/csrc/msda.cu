@@ -19,6 +19,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "../../include/msda.h"
 #include "dcnv4_kernels.cuh"
@@ -34,6 +35,8 @@ struct MGeo {
   int S;                     // value tokens per image
   int H[MSDA_MAX_LEVELS], W[MSDA_MAX_LEVELS], start[MSDA_MAX_LEVELS];
   long long items;           // N * Lq * M
+  long long chunk;           // persistent schedule: slots per CTA per image (0 = flat launch)
+  long long nimg;            // N
 };
 
 // One sample: the four corner element offsets (token*M*D, relative to the item's value
@@ -59,8 +62,17 @@ __device__ __forceinline__ void split_coord(float v, int n, int& i0, float& f, f
   f1 = (float)((fl + 1.0) - w);  // 1 - fraction, also rounded once from the exact value
 }
 
+// a[l] for a runtime level l without dynamic indexing (which would copy the parameter
+// arrays to local memory): a select chain over the MSDA_MAX_LEVELS entries
+__device__ __forceinline__ int lvl(const int (&a)[MSDA_MAX_LEVELS], int l) {
+  int v = a[0];
+#pragma unroll
+  for (int i = 1; i < MSDA_MAX_LEVELS; ++i) v = l == i ? a[i] : v;
+  return v;
+}
+
 __device__ __forceinline__ void corners(const MGeo& g, int l, float x, float y, Corners& c) {
-  const int H = g.H[l], W = g.W[l];
+  const int H = lvl(g.H, l), W = lvl(g.W, l);
   const bool fin = fabsf(x) <= 4096.f && fabsf(y) <= 4096.f;  // NaN / huge: dropped
   int x0, y0;
   float fw, fh, hw, hh;
@@ -79,14 +91,50 @@ __device__ __forceinline__ void corners(const MGeo& g, int l, float x, float y, 
   const float w[4] = {hh * hw, hh * fw, fh * hw, fh * fw};
   const int ys[4] = {y0, y0, y0 + 1, y0 + 1}, xs[4] = {x0, x0 + 1, x0, x0 + 1};
   const unsigned MD = (unsigned)(g.M * g.D);
+  const int st = lvl(g.start, l);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     c.w[q] = c.ok[q] ? w[q] : 0.f;
-    c.o[q] = c.ok[q] ? (unsigned)(g.start[l] + ys[q] * W + xs[q]) * MD : 0u;
+    c.o[q] = c.ok[q] ? (unsigned)(st + ys[q] * W + xs[q]) * MD : 0u;
   }
 }
 
-template <typename T, int NCH, int CPL>
+// The L*P sampling records (x, y, attn) of one item.  LP = L*P > 0 (compile time): read
+// once with 16-B streaming loads (ld.global.cs: loc / attn are touched once, so they
+// should not evict the L2-resident value tensor) and kept in registers; LP = 0: scalar
+// loads at the point of use (any L*P, T-aligned pointers).
+template <typename T, int LP>
+struct ItemSamples {
+  static constexpr int NLV = LP > 0 ? LP * 2 * (int)sizeof(T) / 16 : 1;
+  static constexpr int NAV = LP > 0 ? LP * (int)sizeof(T) / 16 : 1;
+  uint4 lv[NLV], av[NAV];
+  const T* lp;
+  const T* ap;
+  __device__ __forceinline__ void load(const T* l, const T* a) {
+    lp = l;
+    ap = a;
+    if constexpr (LP > 0) {
+#pragma unroll
+      for (int i = 0; i < NLV; ++i) lv[i] = __ldcs(reinterpret_cast<const uint4*>(l) + i);
+#pragma unroll
+      for (int i = 0; i < NAV; ++i) av[i] = __ldcs(reinterpret_cast<const uint4*>(a) + i);
+    }
+  }
+  __device__ __forceinline__ float x(int i) const {
+    if constexpr (LP > 0) return Elem<T>::f(reinterpret_cast<const T*>(lv)[2 * i]);
+    else return Elem<T>::f(lp[2 * i]);
+  }
+  __device__ __forceinline__ float y(int i) const {
+    if constexpr (LP > 0) return Elem<T>::f(reinterpret_cast<const T*>(lv)[2 * i + 1]);
+    else return Elem<T>::f(lp[2 * i + 1]);
+  }
+  __device__ __forceinline__ float a(int i) const {
+    if constexpr (LP > 0) return Elem<T>::f(reinterpret_cast<const T*>(av)[i]);
+    else return Elem<T>::f(ap[i]);
+  }
+};
+
+template <typename T, int NCH, int CPL, int LP>
 __global__ void __launch_bounds__(256) msda_fwd_kernel(MGeo g, const T* __restrict__ value,
                                                        const T* __restrict__ loc,
                                                        const T* __restrict__ attn,
@@ -95,7 +143,7 @@ __global__ void __launch_bounds__(256) msda_fwd_kernel(MGeo g, const T* __restri
   constexpr int E = Elem<T>::E;
   const long long total = g.items * LN;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+  auto body = [&](long long t) {
     const long long item = t / LN;
     const int lg = (int)(t - item * LN);
     const int m = (int)(item % g.M);
@@ -104,36 +152,50 @@ __global__ void __launch_bounds__(256) msda_fwd_kernel(MGeo g, const T* __restri
 #pragma unroll
     for (int h = 0; h < CPL; ++h) co[h] = (h * LN + lg) * E;
     const T* vb = value + ((long long)n * g.S * g.M + m) * g.D;
-    const T* lp = loc + item * g.L * g.P * 2;
-    const T* ap = attn + item * g.L * g.P;
+    ItemSamples<T, LP> smp;
+    smp.load(loc + item * g.L * g.P * 2, attn + item * g.L * g.P);
     float acc[CPL * E];
 #pragma unroll
     for (int e = 0; e < CPL * E; ++e) acc[e] = 0.f;
-    for (int l = 0; l < g.L; ++l) {
+    auto point = [&](int l, int i) {
+      Corners c;
+      corners(g, l, smp.x(i), smp.y(i), c);
+      const float a = smp.a(i);
+      uint4 u[4][CPL];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) u[q][h] = dcnv4::ldg16_idx<sizeof(T)>(vb + co[h], c.o[q]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) dcnv4::fma_chunk<T>(acc + h * E, a * c.w[q], u[q][h]);
+    };
+    if constexpr (LP > 0) {
+#pragma unroll
+      for (int i = 0; i < LP; ++i) point(i / g.P, i);
+    } else {
+      for (int l = 0; l < g.L; ++l) {
 #pragma unroll 2
-      for (int p = 0; p < g.P; ++p) {
-        const int i = l * g.P + p;
-        Corners c;
-        corners(g, l, Elem<T>::f(lp[2 * i]), Elem<T>::f(lp[2 * i + 1]), c);
-        const float a = Elem<T>::f(ap[i]);
-        uint4 u[4][CPL];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int h = 0; h < CPL; ++h) u[q][h] = dcnv4::ldg16_idx<sizeof(T)>(vb + co[h], c.o[q]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int h = 0; h < CPL; ++h) dcnv4::fma_chunk<T>(acc + h * E, a * c.w[q], u[q][h]);
+        for (int p = 0; p < g.P; ++p) point(l, l * g.P + p);
       }
     }
     T* o = out + item * g.D;
 #pragma unroll
-    for (int h = 0; h < CPL; ++h) *reinterpret_cast<uint4*>(o + co[h]) = Elem<T>::pack(acc + h * E);
+    for (int h = 0; h < CPL; ++h) __stcs(reinterpret_cast<uint4*>(o + co[h]), Elem<T>::pack(acc + h * E));
+  };
+  if (g.chunk == 0) {  // flat launch: one (item, lane) slot per thread, blocks in index order
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) body(t);
+  } else {  // persistent: image by image, CTA b owns the contiguous slot range b of each image
+    const long long per_img = total / g.nimg;
+    const long long lo = (long long)blockIdx.x * g.chunk;
+    const long long hi = lo + g.chunk < per_img ? lo + g.chunk : per_img;
+    for (long long n = 0; n < g.nimg; ++n)
+      for (long long b = lo + threadIdx.x; b < hi; b += blockDim.x) body(n * per_img + b);
   }
 }
 
-template <typename T, int NCH, int CPL>
+template <typename T, int NCH, int CPL, int LP>
 __global__ void __launch_bounds__(256) msda_bwd_kernel(MGeo g, const T* __restrict__ value,
                                                        const T* __restrict__ loc,
                                                        const T* __restrict__ attn,
@@ -147,7 +209,7 @@ __global__ void __launch_bounds__(256) msda_bwd_kernel(MGeo g, const T* __restri
   const long long stride = (long long)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
   const unsigned gmask = (LN >= 32 ? 0xffffffffu : ((1u << LN) - 1u)) << (lane & ~(LN - 1));
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+  auto body = [&](long long t) {
     const long long item = t / LN;
     const int lg = (int)(t - item * LN);
     const int m = (int)(item % g.M);
@@ -158,8 +220,8 @@ __global__ void __launch_bounds__(256) msda_bwd_kernel(MGeo g, const T* __restri
     const long long vbase = ((long long)n * g.S * g.M + m) * g.D;
     const T* vb = value + vbase;
     float* gb = gv32 + vbase;
-    const T* lp = loc + item * g.L * g.P * 2;
-    const T* ap = attn + item * g.L * g.P;
+    ItemSamples<T, LP> smp;
+    smp.load(loc + item * g.L * g.P * 2, attn + item * g.L * g.P);
     uint4 gyu[CPL];
     float gyv[CPL * E];
 #pragma unroll
@@ -167,13 +229,11 @@ __global__ void __launch_bounds__(256) msda_bwd_kernel(MGeo g, const T* __restri
       gyu[h] = dcnv4::ld_stream(reinterpret_cast<const uint4*>(gout + item * g.D + co[h]));
       Elem<T>::unpack(gyu[h], gyv + h * E);
     }
-    for (int l = 0; l < g.L; ++l) {
-      const float Wl = (float)g.W[l], Hl = (float)g.H[l];
-      for (int p = 0; p < g.P; ++p) {
-        const int i = l * g.P + p;
+    auto point = [&](int l, int i) {
+        const float Wl = (float)lvl(g.W, l), Hl = (float)lvl(g.H, l);
         Corners c;
-        corners(g, l, Elem<T>::f(lp[2 * i]), Elem<T>::f(lp[2 * i + 1]), c);
-        const float a = Elem<T>::f(ap[i]);
+        corners(g, l, smp.x(i), smp.y(i), c);
+        const float a = smp.a(i);
         float S[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -210,8 +270,23 @@ __global__ void __launch_bounds__(256) msda_bwd_kernel(MGeo g, const T* __restri
                                       aw * gyv[h * E + e + 2], aw * gyv[h * E + e + 3]);
           }
         }
-      }
+    };
+    if constexpr (LP > 0) {
+#pragma unroll
+      for (int i = 0; i < LP; ++i) point(i / g.P, i);
+    } else {
+      for (int l = 0; l < g.L; ++l)
+        for (int p = 0; p < g.P; ++p) point(l, l * g.P + p);
     }
+  };
+  if (g.chunk == 0) {  // flat launch: one (item, lane) slot per thread, blocks in index order
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) body(t);
+  } else {  // persistent: image by image, CTA b owns the contiguous slot range b of each image
+    const long long per_img = total / g.nimg;
+    const long long lo = (long long)blockIdx.x * g.chunk;
+    const long long hi = lo + g.chunk < per_img ? lo + g.chunk : per_img;
+    for (long long n = 0; n < g.nimg; ++n)
+      for (long long b = lo + threadIdx.x; b < hi; b += blockDim.x) body(n * per_img + b);
   }
 }
 
@@ -277,6 +352,8 @@ MGeo make_geo(const msda_params* p, long long S) {
     if (l < p->L) st += p->H[l] * p->W[l];
   }
   g.items = p->N * p->Lq * p->M;
+  g.chunk = 0;
+  g.nimg = p->N;
   return g;
 }
 
@@ -291,23 +368,63 @@ int pick_cpl(int nch) {
   return cpl;
 }
 
+// One thread per (item, lane) slot: blocks are dispatched in index order, so the
+// resident CTAs sweep the images in order and each image's value tensor (20 MB at the
+// Deformable-DETR shape) is read from HBM about once and then hit in L2 by all four
+// query-level segments of the image.  (A capped grid-stride launch keeps eight images in
+// flight and re-reads value from HBM: 2.8x the algorithmic bytes.)  MSDA_GRID_CAP=1
+// restores the capped launch (ablation).
 unsigned grid_for(long long threads) {
   long long b = (threads + 255) / 256;
-  const long long cap = 148LL * 8 * 4;
+  const char* env = getenv("MSDA_GRID_CAP");
+  const long long cap = (env && *env == '1') ? 148LL * 8 * 4 : 0x7fffffffLL;
   return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+// Launch `k` over thr (item, lane) slots.  MSDA_SCHED=persist (ablation): a resident grid
+// (SMs x occupancy) sweeping the images in order, CTA b owning the contiguous slot range b
+// of every image (spatially adjacent queries on one SM share L1 lines); default: the flat
+// launch (grid_for).
+template <typename K, typename... A>
+cudaError_t launch_sched(K k, MGeo g, long long thr, cudaStream_t st, A... args) {
+  const char* env = getenv("MSDA_SCHED");
+  unsigned grid;
+  g.chunk = 0;
+  g.nimg = 1;
+  if (env && env[0] == 'p' && g.items > 0) {
+    int dev = 0, sms = 148, per_sm = 1;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+    g.nimg = g.items / ((long long)g.Lq * g.M);
+    const long long per_img = thr / g.nimg;
+    const long long ctas = (long long)sms * per_sm;
+    long long chunk = (per_img + ctas - 1) / ctas;
+    chunk = (chunk + 255) / 256 * 256;
+    g.chunk = chunk;
+    grid = (unsigned)((per_img + chunk - 1) / chunk);
+  } else {
+    grid = grid_for(thr);
+  }
+  k<<<grid, 256, 0, st>>>(g, args...);
+  return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_fwd(const MGeo& g, int nch, int cpl, const void* v, const void* lo,
                        const void* at, void* out, cudaStream_t st) {
+  // vectorised sample records (L*P = 16, 16-B aligned loc / attn): opt-in, MSDA_VEC=1 --
+  // measured slower than scalar loads (f32 fwd 757 -> 965 us: 80-90 registers)
+  const bool v16 = g.L * g.P == 16 && ((reinterpret_cast<uintptr_t>(lo) | reinterpret_cast<uintptr_t>(at)) & 15) == 0 &&
+                   (getenv("MSDA_VEC") && *getenv("MSDA_VEC") == '1');
   const T* vp = static_cast<const T*>(v);
   const T* lp = static_cast<const T*>(lo);
   const T* ap = static_cast<const T*>(at);
   T* op = static_cast<T*>(out);
   const long long thr = g.items * (nch / cpl);
-  const unsigned grid = grid_for(thr);
-#define MSDA_FWD(NC, CP) \
-  case NC * 100 + CP: msda_fwd_kernel<T, NC, CP><<<grid, 256, 0, st>>>(g, vp, lp, ap, op); break;
+#define MSDA_FWD(NC, CP)                                                                  \
+  case NC * 100 + CP:                                                                     \
+    return v16 ? launch_sched(msda_fwd_kernel<T, NC, CP, 16>, g, thr, st, vp, lp, ap, op)  \
+               : launch_sched(msda_fwd_kernel<T, NC, CP, 0>, g, thr, st, vp, lp, ap, op);
   switch (nch * 100 + cpl) {
     MSDA_FWD(1, 1) MSDA_FWD(2, 1) MSDA_FWD(2, 2) MSDA_FWD(4, 1) MSDA_FWD(4, 2) MSDA_FWD(4, 4)
     MSDA_FWD(8, 1) MSDA_FWD(8, 2) MSDA_FWD(8, 4) MSDA_FWD(16, 1) MSDA_FWD(16, 2) MSDA_FWD(16, 4)
@@ -328,10 +445,12 @@ cudaError_t launch_bwd(const MGeo& g, int nch, int cpl, const void* v, const voi
   T* glp = static_cast<T*>(gl);
   T* gap = static_cast<T*>(ga);
   const long long thr = g.items * (nch / cpl);
-  const unsigned grid = grid_for(thr);
-#define MSDA_BWD(NC, CP)                                                                    \
-  case NC * 100 + CP:                                                                       \
-    msda_bwd_kernel<T, NC, CP><<<grid, 256, 0, st>>>(g, vp, lp, ap, gp, gv, glp, gap); break;
+  const bool v16 = g.L * g.P == 16 && ((reinterpret_cast<uintptr_t>(lo) | reinterpret_cast<uintptr_t>(at)) & 15) == 0 &&
+                   (getenv("MSDA_VEC") && *getenv("MSDA_VEC") == '1');
+#define MSDA_BWD(NC, CP)                                                                          \
+  case NC * 100 + CP:                                                                             \
+    return v16 ? launch_sched(msda_bwd_kernel<T, NC, CP, 16>, g, thr, st, vp, lp, ap, gp, gv, glp, gap) \
+               : launch_sched(msda_bwd_kernel<T, NC, CP, 0>, g, thr, st, vp, lp, ap, gp, gv, glp, gap);
   switch (nch * 100 + cpl) {
     MSDA_BWD(1, 1) MSDA_BWD(2, 1) MSDA_BWD(2, 2) MSDA_BWD(4, 1) MSDA_BWD(4, 2) MSDA_BWD(4, 4)
     MSDA_BWD(8, 1) MSDA_BWD(8, 2) MSDA_BWD(8, 4) MSDA_BWD(16, 1) MSDA_BWD(16, 2) MSDA_BWD(16, 4)
