@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--deterministic", action="store_true",
                     help="bit-reproducible grad_input (int64 fixed point, NEXT-4)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunks", type=int, default=8,
+                    help="image chunks of the host-streaming e2e pipeline (1 = no overlap)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--out", default="", help="also append the JSON line to this file")
@@ -514,35 +516,50 @@ def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
             d2h += sum(h[k].numel() * h[k].element_size() for k in ("gx", "gom"))
         host.append(h)
 
-    def step():
-        for st, h in zip(stages, host):
-            st["x"].copy_(h["x"], non_blocking=True)
-            st["om"].copy_(h["om"], non_blocking=True)
-            pkg.forward(st["x"], st["om"], group=st["G"], softmax=args.softmax, out=st["y"])
-            h["y"].copy_(st["y"], non_blocking=True)
-            if cfg["backward"]:
-                st["gy"].copy_(h["gy"], non_blocking=True)
-                pkg.backward(st["x"], st["om"], st["gy"], group=st["G"], softmax=args.softmax,
-                             grad_input=st["gx"], grad_offset_mask=st["gom"], workspace=st["ws"],
-                             deterministic=args.deterministic)
-                h["gx"].copy_(st["gx"], non_blocking=True)
-                h["gom"].copy_(st["gom"], non_blocking=True)
+    # chunked over images on three streams (paper_2401_06197_b200/pipeline.py): the H2D
+    # copies of chunk c+1, the library calls of chunk c and the D2H copies of chunk c-1
+    # overlap; every byte of every step still crosses the host link inside the timed region
+    from paper_2401_06197_b200.pipeline import HostPipeline
+    nimg = len(stages[0]["x"])
+    nch = max(1, min(args.e2e_chunks, nimg))
+    bounds = [(c * nimg // nch, (c + 1) * nimg // nch) for c in range(nch)]
+    pipe = HostPipeline(dev, nch)
 
-    with torch.cuda.stream(stream):
-        step()
-    stream.synchronize()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
+    def copy_in(c):
+        lo, hi = bounds[c]
+        for st, h in zip(stages, host):
+            st["x"][lo:hi].copy_(h["x"][lo:hi], non_blocking=True)
+            st["om"][lo:hi].copy_(h["om"][lo:hi], non_blocking=True)
+            if cfg["backward"]:
+                st["gy"][lo:hi].copy_(h["gy"][lo:hi], non_blocking=True)
+
+    def compute(c):
+        lo, hi = bounds[c]
+        for st in stages:
+            pkg.forward(st["x"][lo:hi], st["om"][lo:hi], group=st["G"], softmax=args.softmax,
+                        out=st["y"][lo:hi])
+            if cfg["backward"]:
+                pkg.backward(st["x"][lo:hi], st["om"][lo:hi], st["gy"][lo:hi], group=st["G"],
+                             softmax=args.softmax, grad_input=st["gx"][lo:hi],
+                             grad_offset_mask=st["gom"][lo:hi], workspace=st["ws"],
+                             deterministic=args.deterministic)
+
+    def copy_out(c):
+        lo, hi = bounds[c]
+        for st, h in zip(stages, host):
+            h["y"][lo:hi].copy_(st["y"][lo:hi], non_blocking=True)
+            if cfg["backward"]:
+                h["gx"][lo:hi].copy_(st["gx"][lo:hi], non_blocking=True)
+                h["gom"][lo:hi].copy_(st["gom"][lo:hi], non_blocking=True)
+
+    pipe.run(copy_in, compute, copy_out)  # warm-up pass
+    torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with torch.cuda.stream(stream):
-        a.record(stream)
-        for _ in range(args.e2e_steps):
-            step()
-        b.record(stream)
-    stream.synchronize()
-    ms = a.elapsed_time(b) / args.e2e_steps
+    evs = [pipe.run(copy_in, compute, copy_out) for _ in range(args.e2e_steps)]
+    torch.cuda.synchronize(dev)
+    ms = evs[0][0].elapsed_time(evs[-1][1]) / args.e2e_steps
     if ws > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -550,7 +567,8 @@ def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
     n_total = cfg["batch"] if cfg["shard"] else ws * len(stages[0]["x"])
     return {"value": round(n_total / (ms * 1e-3), 2), "unit": "imgs/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": round(ms, 3), "steps": args.e2e_steps}
+            "ms_per_step": round(ms, 3), "steps": args.e2e_steps, "chunks": nch,
+            "overlap": "H2D / kernels / D2H on three streams, chunked by image"}
 
 
 if __name__ == "__main__":
