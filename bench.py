@@ -376,11 +376,19 @@ def main():
             ms = sum(per_call[(si, kind)]) / len(per_call[(si, kind)])
             b = _alg_bytes(st["x"], st["om"], kind == "bwd")
             gbs = b / (ms * 1e-3) / 1e9
+            srt = sorted(per_call[(si, kind)])
+            pick = lambda q: srt[min(len(srt) - 1, int(q * (len(srt) - 1) + 0.5))]  # noqa: E731
             row[f"{kind}_us"] = round(ms * 1e3, 2)
+            row[f"{kind}_us_p10_p50_p90"] = [round(pick(q) * 1e3, 2) for q in (0.1, 0.5, 0.9)]
             row[f"{kind}_GBs"] = round(gbs, 1)
             row[f"{kind}_frac"] = round(gbs / peak, 4)
             kind_bytes[kind] = kind_bytes.get(kind, 0) + b
             kind_ms[kind] = kind_ms.get(kind, 0.0) + ms
+        # checksum: fp64 sums of the outputs of the last step
+        row["checksum"] = {"y": float(st["y"].double().sum())}
+        if cfg["backward"]:
+            row["checksum"]["grad_offset_mask"] = float(st["gom"].double().sum())
+            row["checksum"]["grad_input"] = float(st["gx"].double().sum())
         table.append(row)
     dom = max(kind_ms, key=kind_ms.get)
     launches_dom = len(stages)
