@@ -168,7 +168,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     om_linear_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                      const __grid_constant__ CUtensorMap omap, const T* __restrict__ bias, Args a) {
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(256, 3) module_fwd_kernel(const __grid_constan
   constexpr int RPP = 256 / (TW * GC * L);  // tile rows per aggregation pass
   static_assert(TW * GC * L == 32, "one warp per tile row");
   constexpr int JB = GC * 3 * K;            // om columns of this group block
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
@@ -557,9 +557,12 @@ __global__ void __launch_bounds__(256, 3) module_fwd_kernel(const __grid_constan
   const int gl = (tid / L) % GC;
   const int px = (tid / (L * GC)) % TW;
   const int pyl = tid / (L * GC * TW);
+  // chunk order alternates with the column parity: an 8-lane phase of a 128-bit shared
+  // load (two columns) then covers all eight 16-B bank quads of the 128-B halo pixels
+  const int rot = px & (CPL - 1);
   int co[CPL];
 #pragma unroll
-  for (int h = 0; h < CPL; ++h) co[h] = (h * L + lg) * E;
+  for (int h = 0; h < CPL; ++h) co[h] = (((h + rot) & (CPL - 1)) * L + lg) * E;
   const float s = g.s;
   int sp = 0, sm = 0;
   uint32_t php = 0, phm = 0;
@@ -866,8 +869,44 @@ int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* i
   const int PB = 128;
   g.halo_box_bytes = 22 * 14 * PB;
   g.halo_bytes = (g.halo_box_bytes + 1023) & ~1023;
-  int seg_bytes = (JB * b + 15) & ~15;
-  if ((seg_bytes / 16) % 2 == 0) seg_bytes += 16;
+  // om_s row pitch (4-B multiple) minimising simulated bank conflicts of the epilogue's
+  // row-per-lane u32 stores (32 consecutive pixels) plus the aggregation's scalar reads
+  // (a warp = 8 columns x GC groups x L lanes of one tile row)
+  int seg_bytes = 0, best = 1 << 30;
+  for (int sw = (JB * b + 3) / 4; sw < (JB * b + 3) / 4 + 16; ++sw) {
+    auto ways = [](const int* words, int n) {
+      int w = 1;
+      for (int i = 0; i < n; ++i) {
+        int c = 0;
+        for (int j = 0; j < n; ++j) {
+          bool dup = false;
+          for (int k = 0; k < j; ++k) dup |= words[k] == words[j];
+          if (!dup && words[j] % 32 == words[i] % 32) ++c;
+        }
+        w = c > w ? c : w;
+      }
+      return w;
+    };
+    int words[32], cost = 0;
+    for (int j = 0; j < 4; ++j) {
+      for (int q = 0; q < 32; ++q) words[q] = q * sw + j;
+      cost = cost > ways(words, 32) ? cost : ways(words, 32);
+    }
+    int rc = 0;
+    const int Lg = 32 / (8 * GC);
+    for (int k = 0; k < 27; ++k) {
+      int n = 0;
+      for (int px = 0; px < 8; ++px)
+        for (int gl = 0; gl < GC; ++gl)
+          for (int lg = 0; lg < Lg; ++lg) words[n++] = (px * sw * 4 + gl * 54 + 2 * k) / 4;
+      const int w = ways(words, n);
+      rc = rc > w ? rc : w;
+    }
+    if (cost + rc < best) {
+      best = cost + rc;
+      seg_bytes = sw * 4;
+    }
+  }
   g.seg = seg_bytes / b;
   g.idesc = (1u << 4) | ((dtype == DCNV4_BF16 ? 1u : 0u) << 7) | ((dtype == DCNV4_BF16 ? 1u : 0u) << 10) |
             ((uint32_t)(g.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
