@@ -54,7 +54,7 @@ extern "C" {
 #define DCNV4_API
 #endif
 
-#define DCNV4_VERSION 110 /* 1.1.0: dcnv4_params.deterministic */
+#define DCNV4_VERSION 120 /* 1.2.0: module path (include/dcnv4_module.h); 1.1.0: dcnv4_params.deterministic */
 
 typedef enum { DCNV4_F32 = 0, DCNV4_F16 = 1, DCNV4_BF16 = 2 } dcnv4_dtype;
 
