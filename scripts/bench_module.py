@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--dtype", default="f16", choices=["f16", "bf16"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--weights", default="synth", choices=["synth", "zero"],
+                    help="zero: W = 0, b = 0 (om = 0: zero offsets and masks; ablation)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     N, shapes = STAGES[args.workload]
@@ -51,6 +53,8 @@ def main():
         S = module.om_stride_for(G, K)
         x, _, _ = synth.make_case(N, H, W, G, C // G, H, W, K, 3 * G * K, args.dtype, with_gy=False)
         w, b = synth.make_linear(C, G, K, args.dtype)
+        if args.weights == "zero":
+            w, b = torch.zeros_like(w), torch.zeros_like(b)
         xd, wd, bd = x.to(dev), w.to(dev), b.to(dev)
         om = torch.empty((N, H, W, S), dtype=xd.dtype, device=dev)
         y = torch.empty_like(xd)
@@ -96,7 +100,7 @@ def main():
     line = {"metric": "DCNv4 lightweight module forward: fused kernel (value) vs linear + dcnv4_forward (two_call)",
             "value": round(N / (tot * 1e-6), 2), "unit": "imgs/s",
             "two_call_imgs_s": round(N / (tot2 * 1e-6), 2), "n_gpus": 1, "dtype": args.dtype,
-            "data": "synthetic", "config": {"workload": f"module_{args.workload}", "batch": N, "reps": args.reps,
+            "data": "synthetic", "config": {"workload": f"module_{args.workload}", "batch": N, "reps": args.reps, "weights": args.weights,
                                             "l2": "per-stage working sets up to 0.2 GB; no flush"},
             "peaks": {"hbm_gbs": peak_bw, "tc_tflops": peak_tf, "source": src}, "stages": rows}
     print(json.dumps(line))
