@@ -195,6 +195,85 @@ __global__ void __launch_bounds__(256) msda_fwd_kernel(MGeo g, const T* __restri
   }
 }
 
+// Backward for fp16 / bf16 with 8-byte channel chunks (4 channels per lane): twice the
+// lanes per (query, head) of the 16-B layout, so twice the threads in flight for the
+// latency-bound gather / dot / vector-reduction chain, with the same bytes and the same
+// number of 16-B fp32 reductions per corner (one per lane).  LN = D / 4 lanes per item.
+template <typename T, int LN>
+__global__ void __launch_bounds__(256) msda_bwd8_kernel(MGeo g, const T* __restrict__ value,
+                                                        const T* __restrict__ loc,
+                                                        const T* __restrict__ attn,
+                                                        const T* __restrict__ gout,
+                                                        float* __restrict__ gv32,
+                                                        T* __restrict__ gloc,
+                                                        T* __restrict__ gattn) {
+  const long long total = g.items * LN;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const unsigned gmask = (LN >= 32 ? 0xffffffffu : ((1u << LN) - 1u)) << (lane & ~(LN - 1));
+  auto body = [&](long long t) {
+    const long long item = t / LN;
+    const int lg = (int)(t - item * LN);
+    const int m = (int)(item % g.M);
+    const long long n = item / ((long long)g.M * g.Lq);
+    const int co = lg * 4;
+    const long long vbase = ((long long)n * g.S * g.M + m) * g.D;
+    const T* vb = value + vbase + co;
+    float* gb = gv32 + vbase + co;
+    ItemSamples<T, 0> smp;
+    smp.load(loc + item * g.L * g.P * 2, attn + item * g.L * g.P);
+    const uint2 gu = __ldcs(reinterpret_cast<const uint2*>(gout + item * g.D + co));
+    float gy[4];
+    {
+      const T* gh = reinterpret_cast<const T*>(&gu);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) gy[e] = Elem<T>::f(gh[e]);
+    }
+    for (int l = 0; l < g.L; ++l) {
+      const float Wl = (float)lvl(g.W, l), Hl = (float)lvl(g.H, l);
+      for (int p = 0; p < g.P; ++p) {
+        const int i = l * g.P + p;
+        Corners c;
+        corners(g, l, smp.x(i), smp.y(i), c);
+        const float a = smp.a(i);
+        uint2 u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = __ldg(reinterpret_cast<const uint2*>(vb + c.o[q]));
+        float S[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const T* xh = reinterpret_cast<const T*>(&u[q]);
+          float s0 = 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s0 = fmaf(gy[e], Elem<T>::f(xh[e]), s0);
+          S[q] = c.ok[q] ? s0 : 0.f;
+        }
+        const float hh = c.hh, hw = c.hw;
+        float sa = hh * hw * S[0] + hh * c.fw * S[1] + c.fh * hw * S[2] + c.fh * c.fw * S[3];
+        float sw = hh * (S[1] - S[0]) + c.fh * (S[3] - S[2]);  // d/dw
+        float sh = hw * (S[2] - S[0]) + c.fw * (S[3] - S[1]);  // d/dh
+#pragma unroll
+        for (int o = 1; o < LN; o <<= 1) {
+          sa += __shfl_xor_sync(gmask, sa, o);
+          sw += __shfl_xor_sync(gmask, sw, o);
+          sh += __shfl_xor_sync(gmask, sh, o);
+        }
+        if (lg == 0) {
+          gattn[item * g.L * g.P + i] = Elem<T>::from_f32(sa);
+          gloc[(item * g.L * g.P + i) * 2] = Elem<T>::from_f32(a * Wl * sw);
+          gloc[(item * g.L * g.P + i) * 2 + 1] = Elem<T>::from_f32(a * Hl * sh);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float aw = a * c.w[q];
+          if (aw != 0.f) dcnv4::red_add_v4_idx(gb, c.o[q], aw * gy[0], aw * gy[1], aw * gy[2], aw * gy[3]);
+        }
+      }
+    }
+  };
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) body(t);
+}
+
 template <typename T, int NCH, int CPL, int LP>
 __global__ void __launch_bounds__(256) msda_bwd_kernel(MGeo g, const T* __restrict__ value,
                                                        const T* __restrict__ loc,
@@ -444,6 +523,16 @@ cudaError_t launch_bwd(const MGeo& g, int nch, int cpl, const void* v, const voi
   const T* gp = static_cast<const T*>(go);
   T* glp = static_cast<T*>(gl);
   T* gap = static_cast<T*>(ga);
+  if (sizeof(T) == 2 && !(getenv("MSDA_BWD8") && *getenv("MSDA_BWD8") == '0')) {
+    const long long thr8 = g.items * (g.D / 4);
+    switch (g.D / 4) {
+      case 4: return launch_sched(msda_bwd8_kernel<T, 4>, g, thr8, st, vp, lp, ap, gp, gv, glp, gap);
+      case 8: return launch_sched(msda_bwd8_kernel<T, 8>, g, thr8, st, vp, lp, ap, gp, gv, glp, gap);
+      case 16: return launch_sched(msda_bwd8_kernel<T, 16>, g, thr8, st, vp, lp, ap, gp, gv, glp, gap);
+      case 32: return launch_sched(msda_bwd8_kernel<T, 32>, g, thr8, st, vp, lp, ap, gp, gv, glp, gap);
+      default: break;
+    }
+  }
   const long long thr = g.items * (nch / cpl);
   const bool v16 = g.L * g.P == 16 && ((reinterpret_cast<uintptr_t>(lo) | reinterpret_cast<uintptr_t>(at)) & 15) == 0 &&
                    (getenv("MSDA_VEC") && *getenv("MSDA_VEC") == '1');
