@@ -34,3 +34,27 @@ for (N, H, W, G, D, dt, k, st, pd, dl, sc, off, sm) in cases:
     print("ok", (N, H, W, G, D, dt, k, st, pd, dl, sc, off, sm), float(y.float().abs().sum()),
           float(gx.float().abs().sum()), float(gom.float().abs().sum()),
           float(gxd.float().abs().sum()))
+
+# module path (NEXT-2): tcgen05 linear and the fused module forward (TMA, mbarriers, TMEM)
+from paper_2401_06197_b200 import module, msda  # noqa: E402
+
+for (N, H, W, G, D, dt) in [(1, 20, 13, 8, 16, "f16"), (1, 9, 11, 2, 64, "bf16"), (2, 7, 9, 4, 16, "f16")]:
+    C = G * D
+    x, _, _ = synth.make_case(N, H, W, G, D, H, W, 9, 27 * G, dt, with_gy=False)
+    w, b = synth.make_linear(C, G, 9, dt)
+    x, w, b = x.to(dev), w.to(dev), b.to(dev)
+    om = module.offset_mask_linear(x, w, b, G)
+    y = module.forward_fused(x, w, b, G)
+    torch.cuda.synchronize()
+    print("ok module", (N, H, W, G, D, dt), float(om.float().abs().sum()), float(y.float().abs().sum()))
+
+# MSDA (NEXT-3): forward, 16-B backward (f32) and 8-B half backward
+shapes = ((6, 8), (3, 4), (2, 2))
+for dt in ("f32", "bf16"):
+    S = sum(h * w for h, w in shapes)
+    value, loc, attn, gout = synth.make_msda_case(2, 11, 2, 32, 3, shapes, dt)
+    value, loc, attn, gout = (t.to(dev) for t in (value, loc, attn, gout))
+    out = msda.forward(value, loc, attn, shapes)
+    gv, gl, ga = msda.backward(value, loc, attn, gout, shapes)
+    torch.cuda.synchronize()
+    print("ok msda", dt, float(out.float().abs().sum()), float(gv.float().abs().sum()))
