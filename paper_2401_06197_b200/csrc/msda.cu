@@ -37,6 +37,7 @@ struct MGeo {
   long long items;           // N * Lq * M
   long long chunk;           // persistent schedule: slots per CTA per image (0 = flat launch)
   long long nimg;            // N
+  int qfast;                 // slot order: 1 = queries fastest (see slot_item)
 };
 
 // One sample: the four corner element offsets (token*M*D, relative to the item's value
@@ -134,6 +135,27 @@ struct ItemSamples {
   }
 };
 
+// Slot -> work item.  g.qfast = 0: items in memory order (n, q, m), heads fastest.
+// g.qfast = 1: (n, m, q), queries fastest -- the 32 items of a 256-thread CTA are 32
+// neighbouring queries of ONE head, whose samples land on neighbouring tokens of the same
+// head's value slice (one 128-B line per (token, head) at D*b = 128 B), so the CTA's
+// corner gathers share L1 lines.  Outputs stay whole 128-B lines per item.
+__device__ __forceinline__ void slot_item(const MGeo& g, long long slot, long long& n, int& m,
+                                          long long& item) {
+  if (g.qfast) {
+    const long long per = (long long)g.Lq * g.M;
+    n = slot / per;
+    const long long r = slot - n * per;
+    m = (int)(r / g.Lq);
+    const long long q = r - (long long)m * g.Lq;
+    item = (n * g.Lq + q) * g.M + m;
+  } else {
+    item = slot;
+    m = (int)(slot % g.M);
+    n = slot / ((long long)g.M * g.Lq);
+  }
+}
+
 template <typename T, int NCH, int CPL, int LP>
 __global__ void __launch_bounds__(256) msda_fwd_kernel(MGeo g, const T* __restrict__ value,
                                                        const T* __restrict__ loc,
@@ -144,10 +166,11 @@ __global__ void __launch_bounds__(256) msda_fwd_kernel(MGeo g, const T* __restri
   const long long total = g.items * LN;
   const long long stride = (long long)gridDim.x * blockDim.x;
   auto body = [&](long long t) {
-    const long long item = t / LN;
-    const int lg = (int)(t - item * LN);
-    const int m = (int)(item % g.M);
-    const long long n = item / ((long long)g.M * g.Lq);
+    const long long slot = t / LN;
+    const int lg = (int)(t - slot * LN);
+    int m;
+    long long n, item;
+    slot_item(g, slot, n, m, item);
     int co[CPL];
 #pragma unroll
     for (int h = 0; h < CPL; ++h) co[h] = (h * LN + lg) * E;
@@ -212,10 +235,11 @@ __global__ void __launch_bounds__(256) msda_bwd8_kernel(MGeo g, const T* __restr
   const int lane = threadIdx.x & 31;
   const unsigned gmask = (LN >= 32 ? 0xffffffffu : ((1u << LN) - 1u)) << (lane & ~(LN - 1));
   auto body = [&](long long t) {
-    const long long item = t / LN;
-    const int lg = (int)(t - item * LN);
-    const int m = (int)(item % g.M);
-    const long long n = item / ((long long)g.M * g.Lq);
+    const long long slot = t / LN;
+    const int lg = (int)(t - slot * LN);
+    int m;
+    long long n, item;
+    slot_item(g, slot, n, m, item);
     const int co = lg * 4;
     const long long vbase = ((long long)n * g.S * g.M + m) * g.D;
     const T* vb = value + vbase + co;
@@ -289,10 +313,11 @@ __global__ void __launch_bounds__(256) msda_bwd_kernel(MGeo g, const T* __restri
   const int lane = threadIdx.x & 31;
   const unsigned gmask = (LN >= 32 ? 0xffffffffu : ((1u << LN) - 1u)) << (lane & ~(LN - 1));
   auto body = [&](long long t) {
-    const long long item = t / LN;
-    const int lg = (int)(t - item * LN);
-    const int m = (int)(item % g.M);
-    const long long n = item / ((long long)g.M * g.Lq);
+    const long long slot = t / LN;
+    const int lg = (int)(t - slot * LN);
+    int m;
+    long long n, item;
+    slot_item(g, slot, n, m, item);
     int co[CPL];
 #pragma unroll
     for (int h = 0; h < CPL; ++h) co[h] = (h * LN + lg) * E;
@@ -433,6 +458,8 @@ MGeo make_geo(const msda_params* p, long long S) {
   g.items = p->N * p->Lq * p->M;
   g.chunk = 0;
   g.nimg = p->N;
+  const char* ord = getenv("MSDA_ORDER");
+  g.qfast = (ord && ord[0] == 'q') ? 1 : 0;  // ablation only: measured no better
   return g;
 }
 
