@@ -53,6 +53,14 @@ WORKLOADS = {
     "c5_bf16": dict(desc="BASELINE configs[4]: U-Net 64^2 latents C=320/640/1280, D=16, bf16 "
                          "fwd+bwd, batch 32", stages=STAGES_UNET, dtype="bf16", batch=32,
                     backward=True, shard=False),
+    # NEXT-2 (R21): the lightweight DCNv4 module forward, one fused kernel per
+    # stage (offset/mask linear on tcgen05 + aggregation; om never leaves the SM)
+    "module_c2": dict(desc="NEXT-2 fused lightweight module forward (P:334, P:1003-1009) on the "
+                           "224^2 stage shapes, D=16, fp16, batch 64", stages=STAGES_224,
+                      dtype="f16", batch=64, backward=False, shard=False, module=True),
+    "module_c3": dict(desc="NEXT-2 fused lightweight module forward on the 800x1280 stage "
+                           "shapes, D=16, fp16, batch 8", stages=STAGES_800, dtype="f16", batch=8,
+                      backward=False, shard=False, module=True),
 }
 D = 16
 K = 9
@@ -135,10 +143,13 @@ def _shard(batch, ws, rank, shard):
     return shard_images(batch, ws, rank) if shard else list(range(batch))
 
 
-def _alg_bytes(x, om, backward):
+def _alg_bytes(x, om, backward, w=None):
     """Algorithmic bytes of one call: forward x + om + y; backward
-    x + om + gy (reads) + gx + gom (writes).  y/gy/gx are x-sized, gom is om-sized."""
+    x + om + gy (reads) + gx + gom (writes).  y/gy/gx are x-sized, gom is om-sized.
+    Fused module (w given): x + W + y -- the offset_mask is never in memory."""
     bx = x.numel() * x.element_size()
+    if w is not None:
+        return 2 * bx + w.numel() * w.element_size()
     bo = om.numel() * om.element_size()
     return (3 * bx + 2 * bo) if backward else (2 * bx + bo)
 
@@ -164,6 +175,11 @@ def oracle_inputs(cfg, images):
         g = oracle.Geometry(N=len(images), H=H, W=W, G=G, D=D)
         x, om, gy = synth.make_case(len(images), H, W, G, D, H, W, K, 27 * G, cfg["dtype"],
                                     images=images)
+        if cfg.get("module"):  # om comes from the linear: carry (weight, bias) instead
+            w, b = synth.make_linear(G * D, G, K, cfg["dtype"])
+            om = (oracle._f64(w), oracle._f64(b))
+            data.append((g, oracle._f64(x), om, None))
+            continue
         data.append((g, oracle._f64(x), oracle._f64(om), oracle._f64(gy)))
     return data
 
@@ -174,6 +190,9 @@ def oracle_sample(cfg, data):
     import oracle
     t0 = time.perf_counter()
     for g, x, om, gy in data:
+        if cfg.get("module"):
+            oracle.module_forward(g, x, om[0], om[1], cfg["dtype"])
+            continue
         oracle.forward(g, x, om)
         if cfg["backward"]:
             oracle.backward(g, x, om, gy)
@@ -273,6 +292,9 @@ def main():
                                     images=images, offsets=args.offsets)
         st = dict(H=H, W=W, G=G, x_cpu=x, om_cpu=om, gy_cpu=gy,
                   x=x.to(dev), om=om.to(dev), gy=gy.to(dev))
+        if cfg.get("module"):
+            w, b = synth.make_linear(G * D, G, K, cfg["dtype"])
+            st.update(w_cpu=w, b_cpu=b, w=w.to(dev), b=b.to(dev))
         st["y"] = torch.empty_like(st["x"])
         if cfg["backward"]:
             st["gx"] = torch.empty_like(st["x"])
@@ -285,6 +307,9 @@ def main():
     sm = bool(args.softmax)
 
     def calls(st):
+        if cfg.get("module"):
+            return [("fwd", lambda st=st: pkg.module.forward_fused(st["x"], st["w"], st["b"], st["G"],
+                                                                   softmax=sm, out=st["y"]))]
         out = [("fwd", lambda st=st: pkg.forward(st["x"], st["om"], group=st["G"], softmax=sm,
                                                  out=st["y"]))]
         if cfg["backward"]:
@@ -294,6 +319,13 @@ def main():
         return out
 
     step_calls = [(si, kind, fn) for si, st in enumerate(stages) for kind, fn in calls(st)]
+    flush_bytes = 0
+    if cfg.get("module"):
+        # the module's per-step data (x, y) can fit in L2: flush it (write 2x L2) after every
+        # step; the flush is timed by its own events and excluded from the step time
+        flush_bytes = 256 << 20
+        l2buf = torch.empty(flush_bytes, dtype=torch.uint8, device=dev)
+        step_calls.append((-1, "flush", lambda: l2buf.fill_(1)))
 
     # ---- one eager step (outputs kept for verification outside the timed region)
     stream = torch.cuda.Stream(device=dev)
@@ -353,10 +385,14 @@ def main():
     total_ms = evs[0].elapsed_time(evs[-1])
     durs = [evs[i].elapsed_time(evs[i + 1]) for i in range(len(evs) - 1)]
     per_call = {}
+    flush_ms = 0.0
     for i, d in enumerate(durs):
         si, kind, _ = step_calls[i % n_calls]
+        if kind == "flush":
+            flush_ms += d
+            continue
         per_call.setdefault((si, kind), []).append(d)
-    ms_step_local = total_ms / args.steps
+    ms_step_local = (total_ms - flush_ms) / args.steps
     ms_step = ms_step_local
     if ws > 1:
         t = torch.tensor([ms_step_local], device=dev, dtype=torch.float64)
@@ -374,7 +410,7 @@ def main():
             if (si, kind) not in per_call:
                 continue
             ms = sum(per_call[(si, kind)]) / len(per_call[(si, kind)])
-            b = _alg_bytes(st["x"], st["om"], kind == "bwd")
+            b = _alg_bytes(st["x"], st["om"], kind == "bwd", st.get("w"))
             gbs = b / (ms * 1e-3) / 1e9
             srt = sorted(per_call[(si, kind)])
             pick = lambda q: srt[min(len(srt) - 1, int(q * (len(srt) - 1) + 0.5))]  # noqa: E731
@@ -395,7 +431,8 @@ def main():
     achieved = kind_bytes[dom] / (kind_ms[dom] * 1e-3) / 1e9
     share = kind_ms[dom] / sum(kind_ms.values())
     # every bench workload is 3x3 / stride 1 / dilation 1, i.e. the TMA-halo kernels
-    kname = "memset + bwd33_kernel" if dom == "bwd" else "fwd33_kernel"
+    kname = "memset + bwd33_kernel" if dom == "bwd" else (
+        "module_fwd_kernel: tcgen05 linear + aggregation" if cfg.get("module") else "fwd33_kernel")
     roofline = {"bound": "hbm", "kernel": f"dcnv4 {dom} ({kname}), {launches_dom} launches per step",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
@@ -426,14 +463,17 @@ def main():
                    "grad_input": ("deterministic int64 fixed point" if args.deterministic
                                   else "fp32 atomics") if cfg["backward"] else None,
                    "parallelism": f"batch-sharded dp{ws}" if cfg["shard"] else f"replicas x{ws}",
-                   "l2": f"inputs larger than L2: per-rank working set "
-                         f"{sum(_alg_bytes(s['x'], s['om'], cfg['backward']) for s in stages) / 1e9:.2f} GB "
-                         f"per step vs 126 MB L2; no flush"},
+                   "l2": (f"L2 flushed between steps (a {flush_bytes >> 20} MB write timed "
+                          f"separately and excluded)" if flush_bytes else
+                          f"inputs larger than L2: per-rank working set "
+                          f"{sum(_alg_bytes(s['x'], s['om'], cfg['backward']) for s in stages) / 1e9:.2f} GB "
+                          f"per step vs 126 MB L2; no flush")},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": n_ours * args.steps,
-        "gpu_launch_detail": f"per step: {len(stages)} fwd33_kernel"
+        "gpu_launch_detail": f"per step: {len(stages)} "
+                             + ("module_fwd_kernel" if cfg.get("module") else "fwd33_kernel")
                              + (f" + {len(stages)} bwd33_kernel + {len(stages)} accumulator "
                                 f"zero-fill (cudaMemsetAsync)" if cfg["backward"] else "")
                              + (f" + {len(stages)} det_scale_kernel + {len(stages)} det_convert_kernel"
@@ -465,7 +505,11 @@ def _verify(cfg, stages, images, softmax=False):
     tol = 1e-5 if cfg["dtype"] == "f32" else 1e-2
     for st in stages:
         g = oracle.Geometry(N=1, H=st["H"], W=st["W"], G=st["G"], D=D, softmax=softmax)
-        y_ref, y_abs = oracle.forward(g, st["x_cpu"][:1], st["om_cpu"][:1], with_abs=True)
+        if cfg.get("module"):
+            y_ref, y_abs, _ = oracle.module_forward(g, st["x_cpu"][:1], st["w_cpu"], st["b_cpu"],
+                                                    cfg["dtype"], with_abs=True)
+        else:
+            y_ref, y_abs = oracle.forward(g, st["x_cpu"][:1], st["om_cpu"][:1], with_abs=True)
         errs = {"y": oracle.abs_scaled_error(st["y"][:1].cpu(), y_ref, y_abs)}
         if cfg["backward"]:
             gx_ref, gom_ref, gxa, goma = oracle.backward(g, st["x_cpu"][:1], st["om_cpu"][:1],
@@ -499,7 +543,9 @@ def _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist, sm=F
                 x, om, gy = synth.make_case(1, st["H"], st["W"], st["G"], D, st["H"], st["W"], K,
                                             27 * st["G"], cfg["dtype"], images=[n])
                 x, om, gy = x.to(dev), om.to(dev), gy.to(dev)
-                if key == "y":
+                if key == "y" and cfg.get("module"):
+                    ref = pkg.module.forward_fused(x, st["w"], st["b"], st["G"], softmax=sm)
+                elif key == "y":
                     ref = pkg.forward(x, om, group=st["G"], softmax=sm)
                 else:
                     ref = pkg.backward(x, om, gy, group=st["G"], softmax=sm)[1]
@@ -515,7 +561,9 @@ def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
     for st in stages:
         h = {"x": st["x_cpu"].pin_memory(), "om": st["om_cpu"].pin_memory(),
              "gy": st["gy_cpu"].pin_memory(), "y": torch.empty_like(st["x_cpu"]).pin_memory()}
-        h2d += sum(h[k].numel() * h[k].element_size() for k in ("x", "om"))
+        # module: the offset_mask is computed on the device from x (weights stay resident)
+        h2d += sum(h[k].numel() * h[k].element_size()
+                   for k in (("x",) if cfg.get("module") else ("x", "om")))
         d2h += h["y"].numel() * h["y"].element_size()
         if cfg["backward"]:
             h["gx"] = torch.empty_like(st["x_cpu"]).pin_memory()
@@ -537,13 +585,18 @@ def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
         lo, hi = bounds[c]
         for st, h in zip(stages, host):
             st["x"][lo:hi].copy_(h["x"][lo:hi], non_blocking=True)
-            st["om"][lo:hi].copy_(h["om"][lo:hi], non_blocking=True)
+            if not cfg.get("module"):
+                st["om"][lo:hi].copy_(h["om"][lo:hi], non_blocking=True)
             if cfg["backward"]:
                 st["gy"][lo:hi].copy_(h["gy"][lo:hi], non_blocking=True)
 
     def compute(c):
         lo, hi = bounds[c]
         for st in stages:
+            if cfg.get("module"):
+                pkg.module.forward_fused(st["x"][lo:hi], st["w"], st["b"], st["G"],
+                                         softmax=args.softmax, out=st["y"][lo:hi])
+                continue
             pkg.forward(st["x"][lo:hi], st["om"][lo:hi], group=st["G"], softmax=args.softmax,
                         out=st["y"][lo:hi])
             if cfg["backward"]:

@@ -5,6 +5,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -176,8 +177,43 @@ size_t halo_smem(const dcnv4_params* p, int TH, int TW, int Gc, int b) {
   return 2 * hb + 2 * (size_t)TH * TW * seg_bytes_for(Gc, p->kernel_h * p->kernel_w, b) + 16;
 }
 
+TileChoice choose_tile_search(const dcnv4_params* p, int b, int nch, int cpl, int64_t Ho,
+                              int64_t Wo, bool halo);
+
+// The tile search costs tens of microseconds of host time per call and depends only on
+// the geometry, the chunking and the DCNV4_TILE override: memoised per host thread.
 TileChoice choose_tile(const dcnv4_params* p, int b, int nch, int cpl, int64_t Ho, int64_t Wo,
                        bool halo) {
+  struct Memo {
+    dcnv4_params p;
+    int b, nch, cpl, halo;
+    char env[32];
+    TileChoice tc;
+  };
+  thread_local Memo memo[32];
+  thread_local int memo_n = 0, memo_next = 0;
+  const char* env = getenv("DCNV4_TILE");
+  char ebuf[32] = {0};
+  if (env) snprintf(ebuf, sizeof(ebuf), "%s", env);
+  for (int i = 0; i < memo_n; ++i) {
+    const Memo& m = memo[i];
+    if (m.b == b && m.nch == nch && m.cpl == cpl && m.halo == (int)halo &&
+        memcmp(&m.p, p, sizeof(dcnv4_params)) == 0 && memcmp(m.env, ebuf, sizeof(ebuf)) == 0)
+      return m.tc;
+  }
+  const TileChoice tc = choose_tile_search(p, b, nch, cpl, Ho, Wo, halo);
+  Memo& m = memo[memo_next];
+  memcpy(&m.p, p, sizeof(dcnv4_params));
+  m.b = b; m.nch = nch; m.cpl = cpl; m.halo = (int)halo;
+  memcpy(m.env, ebuf, sizeof(ebuf));
+  m.tc = tc;
+  memo_next = (memo_next + 1) % 32;
+  memo_n = memo_n < 32 ? memo_n + 1 : 32;
+  return tc;
+}
+
+TileChoice choose_tile_search(const dcnv4_params* p, int b, int nch, int cpl, int64_t Ho,
+                              int64_t Wo, bool halo) {
   const int L = nch / cpl;
   const int G = p->G;
   const double V = nch * 16.0;  // bytes of one (pixel, group) channel vector

@@ -9,14 +9,32 @@
 namespace dcnv4 {
 
 // Persistent grid: as many CTAs as fit on the device at once (never more than tiles).
+// The occupancy query costs tens of microseconds of host time; its answer depends only on
+// (device, kernel, threads, shared memory), so it is memoised per host thread.
 static unsigned grid_size(const Launch& lc, const void* kern) {
   if (!lc.persistent) return (unsigned)lc.ctas;
+  struct Memo {
+    const void* kern;
+    int dev, threads, sms, per_sm;
+    size_t smem;
+  };
+  thread_local Memo memo[16];
+  thread_local int memo_n = 0;
   int dev = 0, sms = 148, per_sm = 1;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetDevice(&dev);
+  for (int i = 0; i < memo_n; ++i) {
+    const Memo& m = memo[i];
+    if (m.kern == kern && m.dev == dev && m.threads == lc.threads && m.smem == lc.smem) {
+      const long long g = (long long)m.sms * m.per_sm;
+      return (unsigned)(g < lc.ctas ? g : lc.ctas);
+    }
+  }
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, lc.threads, lc.smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
+  memo[memo_n % 16] = Memo{kern, dev, lc.threads, sms, per_sm, lc.smem};
+  memo_n = memo_n < 16 ? memo_n + 1 : 16;
   const long long g = (long long)sms * per_sm;
   return (unsigned)(g < lc.ctas ? g : lc.ctas);
 }

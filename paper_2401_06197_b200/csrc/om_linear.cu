@@ -765,30 +765,98 @@ dcnv4::FastDiv fastdiv(unsigned d) {  // n / d == (umulhi(n, m) + n) >> l (as dc
   return {(unsigned)(mf - (1ull << 32)), l};
 }
 
+// Row pitch (bytes) of the fused kernel's shared-memory offset_mask tile for GC groups of
+// 27 halves per pixel: the 4-B multiple minimising the worst bank-conflict degree of the
+// epilogue stores (lane = pixel, one u32 each) plus that of the aggregation's reads.
+int seg_pitch(int GC) {
+  const int JB = GC * 27, b = 2;
+  auto ways = [](const int* words, int n) {  // max distinct words mapping to one bank
+    int w = 1;
+    for (int bank = 0; bank < 32; ++bank) {
+      int distinct[32], nd = 0;
+      for (int i = 0; i < n; ++i) {
+        if (words[i] % 32 != bank) continue;
+        bool seen = false;
+        for (int k = 0; k < nd; ++k) seen |= distinct[k] == words[i];
+        if (!seen) distinct[nd++] = words[i];
+      }
+      w = nd > w ? nd : w;
+    }
+    return w;
+  };
+  int best = 1 << 30, pitch = 0;
+  for (int sw = (JB * b + 3) / 4; sw < (JB * b + 3) / 4 + 16; ++sw) {
+    int words[32], cost = 0;
+    for (int j = 0; j < 4; ++j) {
+      for (int q = 0; q < 32; ++q) words[q] = q * sw + j;
+      const int w = ways(words, 32);
+      cost = cost > w ? cost : w;
+    }
+    int rc = 0;
+    const int Lg = 32 / (8 * GC);
+    for (int k = 0; k < 27; ++k) {
+      int n = 0;
+      for (int px = 0; px < 8; ++px)
+        for (int gl = 0; gl < GC; ++gl)
+          for (int lg = 0; lg < Lg; ++lg) words[n++] = (px * sw * 4 + gl * 54 + 2 * k) / 4;
+      const int w = ways(words, n);
+      rc = rc > w ? rc : w;
+    }
+    if (cost + rc < best) {
+      best = cost + rc;
+      pitch = sw * 4;
+    }
+  }
+  return pitch;
+}
+
 template <typename T, int NCH, int CPL>
 cudaError_t launch_module(const CUtensorMap& hm, const CUtensorMap& am, const CUtensorMap& bm, const FGeo& g,
                           bool unit, size_t smem, const void* x, const void* bias, void* y, cudaStream_t st) {
   void (*k)(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
             const __grid_constant__ CUtensorMap, FGeo, const T*, const T*, T*) =
       unit ? module_fwd_kernel<T, NCH, CPL, true> : module_fwd_kernel<T, NCH, CPL, false>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return e;
+  // per-kernel setup (attributes, register count) once per host thread and device
+  struct Memo {
+    const void* k;
+    int dev, regs, sms;
+    size_t smem;
+  };
+  thread_local Memo memo[8];
+  thread_local int memo_n = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int regs_used = -1, sms = 148;
+  for (int i = 0; i < memo_n; ++i)
+    if (memo[i].k == (const void*)k && memo[i].dev == dev && memo[i].smem >= smem) {
+      regs_used = memo[i].regs;
+      sms = memo[i].sms;
+    }
+  cudaError_t e = cudaSuccess;
+  if (regs_used < 0) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa0;
+    e = cudaFuncGetAttributes(&fa0, k);
+    if (e != cudaSuccess) return e;
+    regs_used = fa0.numRegs;
+    sms = num_sms();
+    memo[memo_n % 8] = Memo{(const void*)k, dev, regs_used, sms, smem};
+    memo_n = memo_n < 8 ? memo_n + 1 : 8;
+  }
   // CTAs per SM from registers, shared memory and TMEM columns.  (The occupancy query
   // reports 1 for this kernel; co-residency of 2-3 CTAs was measured to run and to pay:
   // c2 stage 1 143 -> 98 us.)
-  cudaFuncAttributes fa;
-  e = cudaFuncGetAttributes(&fa, k);
-  if (e != cudaSuccess) return e;
-  const int regs = ((fa.numRegs + 7) / 8) * 8 * 256;
+  const int regs = ((regs_used + 7) / 8) * 8 * 256;
   int per_sm = 65536 / (regs > 0 ? regs : 65536);
   const int by_smem = (int)((228 * 1024) / (smem + 1024));
   if (by_smem < per_sm) per_sm = by_smem;
   if ((int)(512 / g.tmem_cols) < per_sm) per_sm = (int)(512 / g.tmem_cols);
   if (const char* f = getenv("DCNV4_MODULE_PER_SM")) per_sm = atoi(f);  // ablation only
   if (per_sm < 1) per_sm = 1;
-  const long long cap = (long long)num_sms() * per_sm;
+  const long long cap = (long long)sms * per_sm;
   const unsigned grid = (unsigned)(g.tiles_total < cap ? g.tiles_total : cap);
   k<<<grid, 256, smem, st>>>(hm, am, bm, g, static_cast<const T*>(x), static_cast<const T*>(bias),
                              static_cast<T*>(y));
@@ -871,42 +939,9 @@ int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* i
   g.halo_bytes = (g.halo_box_bytes + 1023) & ~1023;
   // om_s row pitch (4-B multiple) minimising simulated bank conflicts of the epilogue's
   // row-per-lane u32 stores (32 consecutive pixels) plus the aggregation's scalar reads
-  // (a warp = 8 columns x GC groups x L lanes of one tile row)
-  int seg_bytes = 0, best = 1 << 30;
-  for (int sw = (JB * b + 3) / 4; sw < (JB * b + 3) / 4 + 16; ++sw) {
-    auto ways = [](const int* words, int n) {
-      int w = 1;
-      for (int i = 0; i < n; ++i) {
-        int c = 0;
-        for (int j = 0; j < n; ++j) {
-          bool dup = false;
-          for (int k = 0; k < j; ++k) dup |= words[k] == words[j];
-          if (!dup && words[j] % 32 == words[i] % 32) ++c;
-        }
-        w = c > w ? c : w;
-      }
-      return w;
-    };
-    int words[32], cost = 0;
-    for (int j = 0; j < 4; ++j) {
-      for (int q = 0; q < 32; ++q) words[q] = q * sw + j;
-      cost = cost > ways(words, 32) ? cost : ways(words, 32);
-    }
-    int rc = 0;
-    const int Lg = 32 / (8 * GC);
-    for (int k = 0; k < 27; ++k) {
-      int n = 0;
-      for (int px = 0; px < 8; ++px)
-        for (int gl = 0; gl < GC; ++gl)
-          for (int lg = 0; lg < Lg; ++lg) words[n++] = (px * sw * 4 + gl * 54 + 2 * k) / 4;
-      const int w = ways(words, n);
-      rc = rc > w ? rc : w;
-    }
-    if (cost + rc < best) {
-      best = cost + rc;
-      seg_bytes = sw * 4;
-    }
-  }
+  // (a warp = 8 columns x GC groups x L lanes of one tile row); computed once per GC
+  static const int kSegBytes[3] = {seg_pitch(1), seg_pitch(2), seg_pitch(4)};
+  const int seg_bytes = kSegBytes[GC == 1 ? 0 : GC == 2 ? 1 : 2];
   g.seg = seg_bytes / b;
   g.idesc = (1u << 4) | ((dtype == DCNV4_BF16 ? 1u : 0u) << 7) | ((dtype == DCNV4_BF16 ? 1u : 0u) << 10) |
             ((uint32_t)(g.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
