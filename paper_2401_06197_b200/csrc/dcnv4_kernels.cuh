@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256) fwd_kernel(Geo g, const T* __restrict__ x
   constexpr int L = NCH / CPL;
   constexpr int E = Elem<T>::E;
   constexpr int KC = KH * KW;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   T* const bufs0 = reinterpret_cast<T*>(smem);
   const int bstride = g.TH * g.TW * g.seg;
   const Slot<L, CPL, E> sl(g);
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geo g, const T* __restrict__ x
   constexpr int L = NCH / CPL;
   constexpr int E = Elem<T>::E;
   constexpr int KC = KH * KW;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int npix = g.TH * g.TW;
   T* const bufs0 = reinterpret_cast<T*>(smem);
   const int bstride = npix * g.seg;
