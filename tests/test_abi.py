@@ -58,6 +58,31 @@ def test_offset_mask_linear_validation():
     assert module.om_stride_for(4) == 112 and module.om_stride_for(32) == 864
 
 
+def test_module_forward_validation():
+    """Host-side checks of dcnv4_module_forward (no CUDA call before they pass)."""
+    from paper_2401_06197_b200 import module
+    lib = module._lib()
+    ok = b.make_params(1, 8, 8, 4, 16, 3, 1, 1, 1)
+    nul = (None, None, None, None, None)
+    assert lib.dcnv4_module_forward(ctypes.byref(ok), 0, *nul) == b.ERR_UNSUPPORTED  # F32
+    for bad in (b.make_params(1, 8, 8, 4, 16, 3, 2, 1, 1),   # stride 2
+                b.make_params(1, 8, 8, 4, 16, 5, 1, 2, 1),   # 5x5
+                b.make_params(1, 8, 8, 4, 16, 3, 1, 0, 1),   # pad 0
+                b.make_params(1, 8, 8, 4, 16, 3, 1, 2, 2)):  # dilation 2
+        assert lib.dcnv4_module_forward(ctypes.byref(bad), 1, *nul) == b.ERR_UNSUPPORTED
+        assert b"3x3" in lib.dcnv4_last_error()
+    d8 = b.make_params(1, 8, 8, 8, 8, 3, 1, 1, 1)  # D*2 = 16 B
+    assert lib.dcnv4_module_forward(ctypes.byref(d8), 1, *nul) == b.ERR_UNSUPPORTED
+    g3 = b.make_params(1, 8, 8, 3, 16, 3, 1, 1, 1)  # G not a multiple of GC = 4
+    assert lib.dcnv4_module_forward(ctypes.byref(g3), 2, *nul) == b.ERR_UNSUPPORTED
+    assert lib.dcnv4_module_forward(ctypes.byref(ok), 1, *nul) == b.ERR_INVALID_ARG
+    assert b"input" in lib.dcnv4_last_error()
+    mis = (ctypes.c_void_p(0x1008), ctypes.c_void_p(0x2000), None, ctypes.c_void_p(0x3000), None)
+    assert lib.dcnv4_module_forward(ctypes.byref(ok), 1, *mis) == b.ERR_MISALIGNED
+    empty = b.make_params(0, 8, 8, 4, 16, 3, 1, 1, 1)
+    assert lib.dcnv4_module_forward(ctypes.byref(empty), 1, *nul) == b.OK
+
+
 def test_msda_params_and_validation():
     from paper_2401_06197_b200 import msda
     assert ctypes.sizeof(msda.MSDAParams) == 96
