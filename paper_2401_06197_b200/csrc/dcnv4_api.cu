@@ -555,8 +555,6 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
   if (pass == 0) plan_fwd33(p, dtype, Ho, Wo, x, lc, g);
   else plan_bwd33(p, dtype, Ho, Wo, x, gy, lc, g);
   g->tiles_total = (int)lc->ctas;
-  const char* dbg = getenv("DCNV4_DBG");
-  g->dbg = dbg ? atoi(dbg) : 0;
   const char* np = getenv("DCNV4_NONPERSISTENT");
   lc->persistent = !(np && *np == '1');
   lc->det = pass == 1 && p->deterministic;

@@ -61,7 +61,6 @@ struct Geo {
   // backward (bwd33) shared-memory carve-up (byte offsets) and TMA box of the gy tile
   int gy_box_bytes;
   int o_gy, o_om, o_gom, o_cnt, o_slot, o_ent, o_wsum, o_bar;
-  int dbg;  // profiling only (env DCNV4_DBG): bit0 skips the grad_input phases P2-P4
   // deterministic grad_input (params.deterministic): ceil(log2(Ho*Wo*K)) and the
   // per-image maxima {max|gy|, max|m|} (float bits) written by det_scale_kernel
   int det_lc;
