@@ -436,7 +436,15 @@ int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* i
   const int JB = GC * 27;
   g.BN = (JB + 15) / 16 * 16;
   g.kb = (int)((C + BK - 1) / BK);
-  g.stages = g.kb >= 2 ? 2 : 1;
+  // operand ring: one stage (72 KB of shared memory -> 3 CTAs/SM, other CTAs hide the
+  // k-block loads) up to 4 k blocks (C <= 256); two stages beyond, where a tile's 8
+  // sequential k-block rounds dominate (c2 C=512: 28.7 vs 32.6 us; C=128: 46.9 vs 53.2 us,
+  // profiles/r01b_module_stages_ab.txt).  DCNV4_MODULE_STAGES=1|2 overrides (ablation).
+  g.stages = g.kb <= 4 ? 1 : 2;
+  if (const char* se = getenv("DCNV4_MODULE_STAGES")) {
+    const int v = atoi(se);
+    if (v == 1 || v == 2) g.stages = v <= g.kb ? v : g.stages;
+  }
   g.tiles_h = (int)((p->H + 15) / 16);
   g.tiles_w = (int)((p->W + 7) / 8);
   g.gblocks = p->G / GC;
