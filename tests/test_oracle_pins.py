@@ -490,3 +490,86 @@ def test_thread_count_independence():
         env = dict(os.environ, OMP_NUM_THREADS=t, PYTHONHASHSEED="0")
         outs.add(subprocess.check_output([sys.executable, "-c", code], cwd=root, env=env).strip())
     assert len(outs) == 1
+
+
+# ------------------------------------------------- magnitude scales: equality cases
+def _aim_offsets(g, ty, tx):
+    """Offsets that put sample (pixel, group, tap) at (ty, tx) [N,Ho,Wo,G,K] under the
+    convention sheet (readings R2/R4/R5):
+    py = (ho*sh - ph + cy) + s*(j*dh - cy + dy)."""
+    Ho, Wo = g.out_hw()
+    cy, cx = (g.dh * (g.kh - 1)) // 2, (g.dw * (g.kw - 1)) // 2
+    ho = np.arange(Ho).reshape(1, Ho, 1, 1, 1)
+    wo = np.arange(Wo).reshape(1, 1, Wo, 1, 1)
+    k = np.arange(g.K).reshape(1, 1, 1, 1, g.K)
+    i, j = k // g.kh, k % g.kh
+    dy = (ty - (ho * g.sh - g.ph + cy)) / g.offset_scale - (j * g.dh - cy)
+    dx = (tx - (wo * g.sw - g.pw + cx)) / g.offset_scale - (i * g.dw - cx)
+    return dx, dy
+
+
+@pytest.mark.parametrize("s,softmax", [(1.0, False), (0.5, False), (2.0, False), (1.0, True)])
+@pytest.mark.parametrize("axis", ["y", "x"])
+def test_offset_grad_scale_equals_value_when_terms_agree(s, softmax, axis):
+    """the offset-gradient scale is |s m| sum_c |gy_c| sum_corner |dw| |X|.
+    When every term of grad_d = s m sum_c gy_c sum_corner dw X has the same sign, the
+    scale equals |grad_d| exactly.  For d/dy the corner derivatives are -(1-fx), -fx on
+    the top row and +(1-fx), +fx on the bottom row, so: every sample between rows 2 and 3
+    (top row x <= 0, bottom row x >= 0), gy >= 0, m of either sign (|s m| vs s m flips
+    both).  d/dx likewise with columns 2 | 3.  An inflated or deflated scale (a wrong
+    |s m| factor, a dropped corner) fails here, where an upper-bound check would pass."""
+    g = _g(1, 6, 7, 2, 3, GEOMS[0], s=s, softmax=softmax)
+    Ho, Wo = g.out_hw()
+    rs = np.random.RandomState(41)
+    shape = (g.N, Ho, Wo, g.G, g.K)
+    along = rs.uniform(2.05, 2.95, shape)  # strictly between the split rows/columns
+    across = rs.uniform(0.5, 4.5, shape)
+    ty, tx = (along, across) if axis == "y" else (across, along)
+    dx, dy = _aim_offsets(g, ty, tx)
+    m = rs.uniform(0.2, 1.0, shape) * rs.choice([-1.0, 1.0], shape)
+    u = rs.uniform(0.1, 1.0, (g.N, g.H, g.W, g.C))
+    hh = np.arange(g.H).reshape(1, g.H, 1, 1)
+    ww = np.arange(g.W).reshape(1, 1, g.W, 1)
+    split = hh if axis == "y" else ww
+    x = np.where(split >= 3, u, -u)
+    gy = rs.uniform(0.1, 1.0, (g.N, Ho, Wo, g.C))
+    om = pack_om(dx, dy, m)
+    _, gom, _, goma = oracle.backward(g, x, om, gy, with_abs=True)
+    gdx, gdy, _ = unpack_om(gom, g.G, g.K)
+    adx, ady, _ = unpack_om(goma, g.G, g.K)
+    val, scale = (gdy, ady) if axis == "y" else (gdx, adx)
+    assert np.all(scale > 0)
+    np.testing.assert_allclose(np.abs(val), scale, rtol=1e-12, atol=0)
+
+
+def test_softmax_mask_grad_scale_closed_form():
+    """DCNv3 mode (R18): dL/dz_k = p_k (gm_k - sum_j p_j gm_j); its scale
+    is p_k (|gm|_k + sum_j p_j |gm|_j).  With one tap k0 in the image (the other taps
+    pushed far outside, so gm_k = |gm|_k = 0 for them) and x, gy >= 0, the forward gives
+    <gy, y> = p_k0 gm_k0 per (pixel, group), hence in closed form:
+      k != k0:  scale_k = |grad_k| = p_k <gy, y>,
+      k  = k0:  scale = (1 + p_k0) <gy, y>,  |grad| = (1 - p_k0) <gy, y>."""
+    g = _g(1, 5, 6, 2, 2, GEOMS[0], softmax=True)
+    Ho, Wo = g.out_hw()
+    rs = np.random.RandomState(43)
+    shape = (g.N, Ho, Wo, g.G, g.K)
+    k0 = 4  # centre tap
+    dx = rs.uniform(-0.9, 0.9, shape)
+    dy = rs.uniform(-0.9, 0.9, shape)
+    far = np.arange(g.K) != k0
+    dx[..., far] += 100.0
+    z = rs.uniform(-2, 2, shape)
+    x = rs.uniform(0.1, 1.0, (g.N, g.H, g.W, g.C))
+    gy = rs.uniform(0.1, 1.0, (g.N, Ho, Wo, g.C))
+    om = pack_om(dx, dy, z)
+    y = oracle.forward(g, x, om)
+    _, gom, _, goma = oracle.backward(g, x, om, gy, with_abs=True)
+    gz, az = unpack_om(gom, g.G, g.K)[2], unpack_om(goma, g.G, g.K)[2]
+    e = np.exp(z - z.max(axis=-1, keepdims=True))
+    p = e / e.sum(axis=-1, keepdims=True)  # the DCNv3 normalisation over K (P:196)
+    dot = (gy * y).reshape(g.N, Ho, Wo, g.G, g.D).sum(-1)[..., None]
+    assert np.all(dot > 0)
+    np.testing.assert_allclose(az[..., far], p[..., far] * dot, rtol=1e-12)
+    np.testing.assert_allclose(np.abs(gz[..., far]), az[..., far], rtol=1e-12)
+    np.testing.assert_allclose(az[..., k0], (1 + p[..., k0]) * dot[..., 0], rtol=1e-12)
+    np.testing.assert_allclose(np.abs(gz[..., k0]), (1 - p[..., k0]) * dot[..., 0], rtol=1e-12)
