@@ -6,16 +6,22 @@ operator over the four InternImage-T 224^2 stage shapes (56^2x64 G4, 28^2x128 G8
 14^2x256 G16, 7^2x512 G32; D=16), fp32, forward + backward (every SURVEY.md 8(a) row),
 global batch 512 sharded by batch over the ranks (strong scaling, no collective on the
 data path).  Inputs are seeded synthetic tensors (synth/)
-resident in HBM; the per-rank working set (>= 0.9 GB at 8 ranks) exceeds the 126 MB L2,
-so no flush is needed between timed steps.
+resident in HBM.
 
-Timed region: K steps captured in ONE CUDA graph with external event nodes between the
-library calls, replayed once between a barrier + synchronize on both sides; the step time
-is the max over ranks.  Per-call durations come from those event nodes (on the launching
-stream), giving the per-stage table and the roofline of the dominant kernel.
+Timed region: K steps captured in CUDA graphs with external event nodes between the
+library calls, replayed between a barrier + synchronize on both sides; the step time is
+the max over ranks.  Per-call durations come from those event nodes (on the launching
+stream), giving the per-stage table and the roofline of the dominant kernel.  When a
+step's working set is below 2x L2 a 2xL2 buffer is written after every step (timed by its
+own events and excluded), so no step reads inputs another step left in L2.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2_f32|c2_f16|c3_f16|c5_bf16]
+The default run also measures the forward sweeps (c2, c3 at batch 1 and 8, the paper-
+comparable D=32 shape sets c2'/c3' next to the A100 rows of P:304-305 / P:362-363, and
+c5) and reports them under "forward_sweeps" (--no-extras skips them).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
   python bench.py --impl reference ...   # the fp64 CPU oracle as the reference arm
+--gpus N > 1 outside torchrun re-launches itself under torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -23,6 +29,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -36,10 +43,22 @@ os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
 
 METRIC = ("DCNv4 fwd/bwd µs and HBM GB/s (% of B200 peak) per stage shape; "
           "imgs/s at 1/2/4/8 GPU")
-STAGES_224 = [(56, 56, 4), (28, 28, 8), (14, 14, 16), (7, 7, 32)]
-STAGES_800 = [(200, 320, 4), (100, 160, 8), (50, 80, 16), (25, 40, 32)]
-STAGES_UNET = [(64, 64, 20), (32, 32, 40), (16, 16, 80)]
+# stage shapes (H, W, G, D)
+STAGES_224 = [(56, 56, 4, 16), (28, 28, 8, 16), (14, 14, 16, 16), (7, 7, 32, 16)]
+STAGES_800 = [(200, 320, 4, 16), (100, 160, 8, 16), (50, 80, 16, 16), (25, 40, 32, 16)]
+STAGES_UNET = [(64, 64, 20, 16), (32, 32, 40, 16), (16, 16, 80, 16)]
+# Tab. op_low_res and Tab. op_high_res: group dim 32,
+# batch 64 / 1; the A100 DCNv4 rows (ms, fp32 / fp16) for context
+STAGES_LOW_D32 = [(56, 56, 4, 32), (28, 28, 8, 32), (14, 14, 16, 32), (7, 7, 32, 32), (14, 14, 24, 32)]
+STAGES_HIGH_D32 = [(200, 320, 4, 32), (100, 160, 8, 32), (50, 80, 16, 32), (25, 40, 32, 32),
+                   (64, 64, 24, 32)]
+PAPER_A100_MS = {
+    "low": {"f32": [0.606, 0.303, 0.145, 0.0730, 0.224], "f16": [0.404, 0.230, 0.123, 0.0680, 0.147]},
+    "high": {"f32": [0.210, 0.124, 0.0707, 0.0452, 0.103], "f16": [0.136, 0.0895, 0.0589, 0.0426, 0.0672]},
+}
 WORKLOADS = {
+    "c1": dict(desc="BASELINE configs[0]: tiny 8x8x32 G2 D16 fp32 fwd+bwd (parity case)",
+               stages=[(8, 8, 2, 16)], dtype="f32", batch=1, backward=True, shard=True),
     "c4": dict(desc="BASELINE configs[3]: training fwd+bwd, InternImage-T 224^2 four-stage "
                     "shapes, D=16, fp32, global batch 512 sharded by batch",
                stages=STAGES_224, dtype="f32", batch=512, backward=True, shard=True),
@@ -53,6 +72,18 @@ WORKLOADS = {
     "c5_bf16": dict(desc="BASELINE configs[4]: U-Net 64^2 latents C=320/640/1280, D=16, bf16 "
                          "fwd+bwd, batch 32", stages=STAGES_UNET, dtype="bf16", batch=32,
                     backward=True, shard=False),
+    "c2p_f32": dict(desc="c2' (SURVEY 8(d).1): Tab. op_low_res shapes, D=32, fp32 forward, batch 64",
+                    stages=STAGES_LOW_D32, dtype="f32", batch=64, backward=False, shard=False,
+                    paper="low"),
+    "c2p_f16": dict(desc="c2' (SURVEY 8(d).1): Tab. op_low_res shapes, D=32, fp16 forward, batch 64",
+                    stages=STAGES_LOW_D32, dtype="f16", batch=64, backward=False, shard=False,
+                    paper="low"),
+    "c3p_f32": dict(desc="c3' (SURVEY 8(d).1): Tab. op_high_res shapes, D=32, fp32 forward, batch 1",
+                    stages=STAGES_HIGH_D32, dtype="f32", batch=1, backward=False, shard=False,
+                    paper="high"),
+    "c3p_f16": dict(desc="c3' (SURVEY 8(d).1): Tab. op_high_res shapes, D=32, fp16 forward, batch 1",
+                    stages=STAGES_HIGH_D32, dtype="f16", batch=1, backward=False, shard=False,
+                    paper="high"),
     # NEXT-2 (R21): the lightweight DCNv4 module forward, one fused kernel per
     # stage (offset/mask linear on tcgen05 + aggregation; om never leaves the SM)
     "module_c2": dict(desc="NEXT-2 fused lightweight module forward (P:334, P:1003-1009) on the "
@@ -62,8 +93,12 @@ WORKLOADS = {
                            "shapes, D=16, fp16, batch 8", stages=STAGES_800, dtype="f16", batch=8,
                       backward=False, shard=False, module=True),
 }
-D = 16
+# forward sweeps measured by the default run (workload, batch override)
+EXTRAS = [("c2_f32", None), ("c2_f16", None), ("c3_f16", 1), ("c3_f16", 8), ("c2p_f32", None),
+          ("c2p_f16", None), ("c3p_f32", None), ("c3p_f16", None), ("c5_bf16", None)]
 K = 9
+MIN_TIMED_S = 0.4      # auto step count: timed region >= this (>= 2 clock samples at 50 ms)
+GRAPH_STEPS = 100      # steps per captured graph (longer regions replay it)
 
 
 def _peaks():
@@ -73,6 +108,10 @@ def _peaks():
         return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def shape_name(H, W, G, D):
+    return f"{H}x{W}x{G * D} G{G} D{D}"
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -114,7 +153,8 @@ class ClockSampler:
 
     def summary(self, t0: float, t1: float):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0,
+                    "samples_in_timed_region": 0}
         inside = [s for t, s in self.samples if t0 <= t <= t1]
         use = inside or [min(self.samples, key=lambda ts: abs(ts[0] - (t0 + t1) / 2))[1]]
 
@@ -132,7 +172,7 @@ class ClockSampler:
                 "power_w_max": max((num(s[3]) or 0.0) for s in use)}
 
 
-# ----------------------------------------------------------------------------- helpers
+# ----------------------------------------------------------------------------- multi-rank host logic
 def _dist():
     from paper_2401_06197_b200.sharding import dist_env
     return dist_env()
@@ -143,6 +183,59 @@ def _shard(batch, ws, rank, shard):
     return shard_images(batch, ws, rank) if shard else list(range(batch))
 
 
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(nproc: int, argv) -> int:
+    """`--gpus N` outside torchrun: re-run this script under torch.distributed.run with N
+    ranks on this node (rendezvous on 127.0.0.1), NCCL init logging on; returns the exit
+    status of the launcher (rank 0 prints the JSON line)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
+def max_over_ranks(v: float, ws: int, dist, device) -> float:
+    """The slowest rank's value (step times are reported as the max over ranks)."""
+    if ws <= 1:
+        return v
+    import torch
+    t = torch.tensor([v], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cross_rank_check(first_image: int, outputs, recompute, ws: int, rank: int, dist, device):
+    """N > 1: gather every rank's first-image outputs (a list of tensors, one per
+    (stage, tensor)) to rank 0, which recomputes those images alone with
+    recompute(image, index) and requires bit-identical results (forward and
+    grad_offset_mask do not depend on the batch partition, R14).
+    Returns {"cross_rank_bitexact": bool, "ranks": ws} on rank 0, None elsewhere."""
+    import torch
+    first = torch.tensor([first_image], device=device, dtype=torch.int64)
+    firsts = [torch.zeros_like(first) for _ in range(ws)]
+    dist.all_gather(firsts, first)
+    ok = True
+    for idx, mine in enumerate(outputs):
+        mine = mine.contiguous()
+        got = [torch.empty_like(mine) for _ in range(ws)] if rank == 0 else None
+        dist.gather(mine, got, dst=0)
+        if rank != 0:
+            continue
+        for r in range(ws):
+            ref = recompute(int(firsts[r].item()), idx)
+            ok = ok and bool(torch.equal(ref.to(got[r].device), got[r]))
+    return {"cross_rank_bitexact": ok, "ranks": ws} if rank == 0 else None
+
+
+# ----------------------------------------------------------------------------- bytes
 def _alg_bytes(x, om, backward, w=None):
     """Algorithmic bytes of one call: forward x + om + y; backward
     x + om + gy (reads) + gx + gom (writes).  y/gy/gx are x-sized, gom is om-sized.
@@ -171,7 +264,7 @@ def oracle_inputs(cfg, images):
     import synth
     oracle.build()
     data = []
-    for (H, W, G) in cfg["stages"]:
+    for (H, W, G, D) in cfg["stages"]:
         g = oracle.Geometry(N=len(images), H=H, W=W, G=G, D=D)
         x, om, gy = synth.make_case(len(images), H, W, G, D, H, W, K, 27 * G, cfg["dtype"],
                                     images=images)
@@ -214,18 +307,19 @@ def run_reference(args, cfg):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
+    steps = args.steps or 2
     budget = 60.0
     t2 = oracle_sample(cfg, oracle_inputs(cfg, [0, 1])) / 2
-    n = int(max(1, min(cfg["batch"], budget / max(1, args.steps + args.warmup) / max(t2, 1e-3))))
+    n = int(max(1, min(cfg["batch"], budget / max(1, steps + args.warmup) / max(t2, 1e-3))))
     data = oracle_inputs(cfg, list(range(n)))
     for _ in range(args.warmup):
         oracle_sample(cfg, data)
-    times = [oracle_sample(cfg, data) for _ in range(args.steps)]
+    times = [oracle_sample(cfg, data) for _ in range(steps)]
     tot = sum(times)
-    value = n * args.steps / tot
+    value = n * steps / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "imgs/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / steps,
         "higher_is_better": True, "scaling": "strong" if cfg["shard"] else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["name"], "desc": cfg["desc"], "global_batch": cfg["batch"],
@@ -242,56 +336,31 @@ def run_reference(args, cfg):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
-    ap.add_argument("--global-batch", type=int, default=0)
-    ap.add_argument("--offsets", default="u2", choices=["u2", "zero", "u8", "smooth"])
-    ap.add_argument("--softmax", action="store_true",
-                    help="DCNv3 mode (softmax over K, NEXT-1) instead of DCNv4")
-    ap.add_argument("--deterministic", action="store_true",
-                    help="bit-reproducible grad_input (int64 fixed point, NEXT-4)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-chunks", type=int, default=8,
-                    help="image chunks of the host-streaming e2e pipeline (1 = no overlap)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-verify", action="store_true")
-    ap.add_argument("--out", default="", help="also append the JSON line to this file")
-    args = ap.parse_args()
-    cfg = dict(WORKLOADS[args.workload], name=args.workload)
-    if args.global_batch:
-        cfg["batch"] = args.global_batch
-    if args.warmup < 3:
-        args.warmup = 3  # contract: >= 3 untimed warm-up steps
-    if args.impl == "reference":
-        return run_reference(args, cfg)
+class Ctx:
+    """Per-process run context (device, ranks, streams, clock sampler)."""
 
-    import torch
-    import torch.distributed as dist
+    def __init__(self, torch, dist, pkg, dev, ws, rank):
+        self.torch, self.dist, self.pkg, self.dev, self.ws, self.rank = torch, dist, pkg, dev, ws, rank
+        self.stream = torch.cuda.Stream(device=dev)
+        self.l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+        uuid = None
+        try:
+            uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+        except Exception:
+            pass
+        self.sampler = ClockSampler(uuid)
 
+
+def _make_stages(cfg, ctx, images, offsets, deterministic):
     import synth
-    import paper_2401_06197_b200 as pkg
-
-    ws, rank, local = _dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    images = _shard(cfg["batch"], ws, rank, cfg["shard"])
-    n_img = len(images)
+    torch, pkg, dev = ctx.torch, ctx.pkg, ctx.dev
     tdt = synth.DTYPES[cfg["dtype"]]
-
-    # ---- resident inputs / outputs (per-image seeds: any world size sees the same images)
     stages = []
-    for (H, W, G) in cfg["stages"]:
-        x, om, gy = synth.make_case(n_img, H, W, G, D, H, W, K, 27 * G, cfg["dtype"],
-                                    images=images, offsets=args.offsets)
-        st = dict(H=H, W=W, G=G, x_cpu=x, om_cpu=om, gy_cpu=gy,
-                  x=x.to(dev), om=om.to(dev), gy=gy.to(dev))
+    for (H, W, G, D) in cfg["stages"]:
+        x, om, gy = synth.make_case(len(images), H, W, G, D, H, W, K, 27 * G, cfg["dtype"],
+                                    images=images, offsets=offsets, with_gy=cfg["backward"])
+        st = dict(H=H, W=W, G=G, D=D, x_cpu=x, om_cpu=om, gy_cpu=gy, x=x.to(dev), om=om.to(dev),
+                  gy=gy.to(dev) if gy is not None else None)
         if cfg.get("module"):
             w, b = synth.make_linear(G * D, G, K, cfg["dtype"])
             st.update(w_cpu=w, b_cpu=b, w=w.to(dev), b=b.to(dev))
@@ -299,61 +368,84 @@ def main():
         if cfg["backward"]:
             st["gx"] = torch.empty_like(st["x"])
             st["gom"] = torch.empty_like(st["om"])
-            need = pkg.workspace_bytes(pkg.make_params(n_img, H, W, G, D,
-                                                       deterministic=args.deterministic), tdt)
+            need = pkg.workspace_bytes(pkg.make_params(len(images), H, W, G, D,
+                                                       deterministic=deterministic), tdt)
             st["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         stages.append(st)
+    return stages
 
-    sm = bool(args.softmax)
 
-    def calls(st):
-        if cfg.get("module"):
-            return [("fwd", lambda st=st: pkg.module.forward_fused(st["x"], st["w"], st["b"], st["G"],
-                                                                   softmax=sm, out=st["y"]))]
-        out = [("fwd", lambda st=st: pkg.forward(st["x"], st["om"], group=st["G"], softmax=sm,
-                                                 out=st["y"]))]
-        if cfg["backward"]:
-            out.append(("bwd", lambda st=st: pkg.backward(
-                st["x"], st["om"], st["gy"], group=st["G"], softmax=sm, grad_input=st["gx"],
-                grad_offset_mask=st["gom"], workspace=st["ws"], deterministic=args.deterministic)))
-        return out
-
-    step_calls = [(si, kind, fn) for si, st in enumerate(stages) for kind, fn in calls(st)]
-    flush_bytes = 0
+def _calls(cfg, st, pkg, softmax, deterministic):
     if cfg.get("module"):
-        # the module's per-step data (x, y) can fit in L2: flush it (write 2x L2) after every
-        # step; the flush is timed by its own events and excluded from the step time
-        flush_bytes = 256 << 20
+        return [("fwd", lambda: pkg.module.forward_fused(st["x"], st["w"], st["b"], st["G"],
+                                                         softmax=softmax, out=st["y"]))]
+    out = [("fwd", lambda: pkg.forward(st["x"], st["om"], group=st["G"], softmax=softmax,
+                                       out=st["y"]))]
+    if cfg["backward"]:
+        out.append(("bwd", lambda: pkg.backward(
+            st["x"], st["om"], st["gy"], group=st["G"], softmax=softmax, grad_input=st["gx"],
+            grad_offset_mask=st["gom"], workspace=st["ws"], deterministic=deterministic)))
+    return out
+
+
+def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, deterministic=False,
+            verify=True):
+    """Time `steps` steps of workload `cfg` on this rank's `images`; returns a dict with the
+    max-over-ranks step time, the per-stage table, the dominant kernel's roofline, the
+    clocks sampled during the timed region and the parity record."""
+    torch, pkg, dev, stream, ws, rank = ctx.torch, ctx.pkg, ctx.dev, ctx.stream, ctx.ws, ctx.rank
+    stages = _make_stages(cfg, ctx, images, offsets, deterministic)
+    step_calls = [(si, kind, fn) for si, st in enumerate(stages)
+                  for kind, fn in _calls(cfg, st, pkg, softmax, deterministic)]
+    work_set = sum(_alg_bytes(s["x"], s["om"], cfg["backward"], s.get("w")) for s in stages)
+    flush_bytes = 0
+    if work_set < 2 * ctx.l2_bytes:
+        # the step's data could stay in L2 between steps: write a 2xL2 buffer after every
+        # step (timed by its own events and excluded from the step time)
+        flush_bytes = 2 * ctx.l2_bytes
         l2buf = torch.empty(flush_bytes, dtype=torch.uint8, device=dev)
         step_calls.append((-1, "flush", lambda: l2buf.fill_(1)))
 
-    # ---- one eager step (outputs kept for verification outside the timed region)
-    stream = torch.cuda.Stream(device=dev)
+    # one eager step (outputs kept for verification outside the timed region)
     with torch.cuda.stream(stream):
         for _, _, fn in step_calls:
             fn()
     stream.synchronize()
-    verify = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.no_verify:
-        # cpu_baseline leg (the only place bench.py runs oracle/): first image vs fp64 oracle
-        verify = _verify(cfg, stages, images, softmax=sm)
-    elif ws > 1 and not args.no_verify:
-        verify = _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist, sm)
+    parity = None
+    if verify and ws == 1:
+        parity = _verify(cfg, stages, images, softmax=softmax)
+    elif verify and ws > 1:
+        parity = _cross_rank(cfg, stages, images, ctx, softmax)
 
-    # ---- warm-up (eager), then capture K steps with event nodes between calls
+    # warm-up (eager), then capture up to GRAPH_STEPS steps with event nodes between calls
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             for _, _, fn in step_calls:
                 fn()
     stream.synchronize()
+    if steps is None:  # auto: a timed region of >= MIN_TIMED_S, in whole graphs
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            for _, _, fn in step_calls:
+                fn()
+            b.record(stream)
+        stream.synchronize()
+        est = max(a.elapsed_time(b), 1e-3)
+        steps = max(20, math.ceil(MIN_TIMED_S * 1e3 / est))
+        if steps > GRAPH_STEPS:
+            steps = math.ceil(steps / GRAPH_STEPS) * GRAPH_STEPS
+    gsteps = steps if steps <= GRAPH_STEPS else GRAPH_STEPS
+    if steps % gsteps:
+        raise ValueError(f"--steps {steps} > {GRAPH_STEPS} must be a multiple of {GRAPH_STEPS}")
+    replays = steps // gsteps
     n_calls = len(step_calls)
-    evs = [torch.cuda.Event(enable_timing=True, external=True)
-           for _ in range(args.steps * n_calls + 1)]
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(gsteps * n_calls + 1)]
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         evs[0].record(stream)
         e = 1
-        for _ in range(args.steps):
+        for _ in range(gsteps):
             for _, _, fn in step_calls:
                 fn()
                 evs[e].record(stream)
@@ -361,29 +453,27 @@ def main():
     graph.replay()  # one untimed replay (graph upload, warm)
     stream.synchronize()
 
-    uuid = None
-    try:
-        uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
-    except Exception:
-        pass
-    sampler = ClockSampler(uuid)
-    time.sleep(0.3)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    time.sleep(0.2)
     if ws > 1:
-        dist.barrier()
+        ctx.dist.barrier()
     torch.cuda.synchronize(dev)
     t_wall0 = time.time()
     with torch.cuda.stream(stream):
-        graph.replay()
+        t_start.record(stream)
+        for _ in range(replays):
+            graph.replay()
+        t_end.record(stream)
     torch.cuda.synchronize(dev)
     t_wall1 = time.time()
     if ws > 1:
-        dist.barrier()
+        ctx.dist.barrier()
     time.sleep(0.1)
-    sampler.stop()
-    clocks = sampler.summary(t_wall0, t_wall1)
+    clocks = ctx.sampler.summary(t_wall0, t_wall1)
 
-    total_ms = evs[0].elapsed_time(evs[-1])
-    durs = [evs[i].elapsed_time(evs[i + 1]) for i in range(len(evs) - 1)]
+    total_ms = t_start.elapsed_time(t_end)
+    durs = [evs[i].elapsed_time(evs[i + 1]) for i in range(len(evs) - 1)]  # last replay
     per_call = {}
     flush_ms = 0.0
     for i, d in enumerate(durs):
@@ -392,20 +482,15 @@ def main():
             flush_ms += d
             continue
         per_call.setdefault((si, kind), []).append(d)
-    ms_step_local = (total_ms - flush_ms) / args.steps
-    ms_step = ms_step_local
-    if ws > 1:
-        t = torch.tensor([ms_step_local], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    value = cfg["batch"] / (ms_step * 1e-3) if cfg["shard"] else ws * n_img / (ms_step * 1e-3)
+    flush_per_step = flush_ms / gsteps
+    ms_step = max_over_ranks((total_ms - flush_per_step * steps) / steps, ws, ctx.dist, dev)
 
-    # ---- per-stage table and roofline of the dominant kernel
     peak, peak_src = _peaks()
     table = []
     kind_bytes, kind_ms = {}, {}
+    paper = PAPER_A100_MS.get(cfg.get("paper"), {}).get(cfg["dtype"])
     for si, st in enumerate(stages):
-        row = {"shape": f"{st['H']}x{st['W']}x{st['G'] * D} G{st['G']}", "images": n_img}
+        row = {"shape": shape_name(st["H"], st["W"], st["G"], st["D"]), "images": len(images)}
         for kind in ("fwd", "bwd"):
             if (si, kind) not in per_call:
                 continue
@@ -420,6 +505,8 @@ def main():
             row[f"{kind}_frac"] = round(gbs / peak, 4)
             kind_bytes[kind] = kind_bytes.get(kind, 0) + b
             kind_ms[kind] = kind_ms.get(kind, 0.0) + ms
+        if paper and si < len(paper):
+            row["paper_a100_fwd_us"] = round(paper[si] * 1e3, 1)
         # checksum: fp64 sums of the outputs of the last step
         row["checksum"] = {"y": float(st["y"].double().sum())}
         if cfg["backward"]:
@@ -430,7 +517,6 @@ def main():
     launches_dom = len(stages)
     achieved = kind_bytes[dom] / (kind_ms[dom] * 1e-3) / 1e9
     share = kind_ms[dom] / sum(kind_ms.values())
-    # every bench workload is 3x3 / stride 1 / dilation 1, i.e. the TMA-halo kernels
     kname = "memset + bwd33_kernel" if dom == "bwd" else (
         "module_fwd_kernel: tcgen05 linear + aggregation" if cfg.get("module") else "fwd33_kernel")
     roofline = {"bound": "hbm", "kernel": f"dcnv4 {dom} ({kname}), {launches_dom} launches per step",
@@ -438,73 +524,23 @@ def main():
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "traffic": _traffic(cfg["name"], dom), "share_of_step": round(share, 4),
                 "alg_bytes_per_launch": int(kind_bytes[dom] / launches_dom)}
-
-    # ---- end to end through the public API with pinned host buffers
-    e2e = _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist)
-
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
-
-    n_ours = (2 if cfg["backward"] else 1) * len(stages)
-    if cfg["backward"] and args.deterministic:
-        n_ours += 2 * len(stages)  # per-image maxima + int64 -> T conversion
-    elif cfg["backward"] and cfg["dtype"] != "f32":
-        n_ours += len(stages)  # fp32 -> half grad_input conversion
-    line = {
-        "metric": METRIC, "value": round(value, 2), "unit": "imgs/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-        "higher_is_better": True, "scaling": "strong" if cfg["shard"] else "weak",
-        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
-        "config": {"workload": cfg["name"], "desc": cfg["desc"], "global_batch": cfg["batch"],
-                   "per_gpu_batch": n_img, "stages": [f"{h}x{w}x{g * D} G{g}" for h, w, g in cfg["stages"]],
-                   "D": D, "kernel": "3x3 s1 p1 d1", "offset_scale": 1.0, "offsets": args.offsets,
-                   "operator": "DCNv3 (softmax over K)" if sm else "DCNv4",
-                   "grad_input": ("deterministic int64 fixed point" if args.deterministic
-                                  else "fp32 atomics") if cfg["backward"] else None,
-                   "parallelism": f"batch-sharded dp{ws}" if cfg["shard"] else f"replicas x{ws}",
-                   "l2": (f"L2 flushed between steps (a {flush_bytes >> 20} MB write timed "
-                          f"separately and excluded)" if flush_bytes else
-                          f"inputs larger than L2: per-rank working set "
-                          f"{sum(_alg_bytes(s['x'], s['om'], cfg['backward']) for s in stages) / 1e9:.2f} GB "
-                          f"per step vs 126 MB L2; no flush")},
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": n_ours * args.steps,
-        "gpu_launch_detail": f"per step: {len(stages)} "
-                             + ("module_fwd_kernel" if cfg.get("module") else "fwd33_kernel")
-                             + (f" + {len(stages)} bwd33_kernel + {len(stages)} accumulator "
-                                f"zero-fill (cudaMemsetAsync)" if cfg["backward"] else "")
-                             + (f" + {len(stages)} det_scale_kernel + {len(stages)} det_convert_kernel"
-                                if cfg["backward"] and args.deterministic else
-                                f" + {len(stages)} convert_kernel" if cfg["backward"] and cfg["dtype"] != "f32"
-                                else ""),
-        "clocks": clocks,
-        "stages": table,
-        "parity": verify,
-        "wall_s_timed_region": round(t_wall1 - t_wall0, 4),
-    }
-    if rank == 0:
-        s = json.dumps(line)
-        print(s, flush=True)
-        if args.out:
-            with open(args.out, "a") as f:
-                f.write(s + "\n")
-    if ws > 1:
-        dist.barrier()
-        dist.destroy_process_group()
-    return 0
+    l2 = (f"step working set {work_set / 1e6:.1f} MB < 2x L2 ({2 * ctx.l2_bytes >> 20} MB): "
+          f"a {flush_bytes >> 20} MB buffer written after every step, timed separately and "
+          f"excluded" if flush_bytes else
+          f"inputs larger than L2: step working set {work_set / 1e9:.2f} GB vs "
+          f"{ctx.l2_bytes >> 20} MB L2; no flush")
+    return {"stages": stages, "ms_step": ms_step, "steps": steps, "table": table,
+            "roofline": roofline, "clocks": clocks, "parity": parity, "l2": l2,
+            "wall_s": round(t_wall1 - t_wall0, 4), "replays": replays}
 
 
 def _verify(cfg, stages, images, softmax=False):
     """Oracle check of the shard's first image on every stage (outside the timed region)."""
-    import numpy as np
     import oracle
     out = {}
     tol = 1e-5 if cfg["dtype"] == "f32" else 1e-2
     for st in stages:
-        g = oracle.Geometry(N=1, H=st["H"], W=st["W"], G=st["G"], D=D, softmax=softmax)
+        g = oracle.Geometry(N=1, H=st["H"], W=st["W"], G=st["G"], D=st["D"], softmax=softmax)
         if cfg.get("module"):
             y_ref, y_abs, _ = oracle.module_forward(g, st["x_cpu"][:1], st["w_cpu"], st["b_cpu"],
                                                     cfg["dtype"], with_abs=True)
@@ -516,56 +552,46 @@ def _verify(cfg, stages, images, softmax=False):
                                                          st["gy_cpu"][:1], with_abs=True)
             errs["grad_input"] = oracle.abs_scaled_error(st["gx"][:1].cpu(), gx_ref, gxa)
             errs["grad_offset_mask"] = oracle.abs_scaled_error(st["gom"][:1].cpu(), gom_ref, goma)
-        out[f"{st['H']}x{st['W']}"] = {k: float(f"{v:.3e}") for k, v in errs.items()}
+        out[shape_name(st["H"], st["W"], st["G"], st["D"])] = {k: float(f"{v:.3e}") for k, v in errs.items()}
     worst = max(v for e in out.values() for v in e.values())
     return {"image": images[0], "max_abs_scaled_error": worst, "tol": tol,
             "pass": bool(worst <= tol), "per_stage": out}
 
 
-def _cross_rank_check(cfg, stages, images, dev, ws, rank, pkg, torch, dist, sm=False):
-    """N > 1: gather (NCCL) every rank's first-image y and grad_offset_mask to rank 0, which
-    recomputes those images alone and requires bit-identical results (forward and
-    grad_offset_mask do not depend on the batch partition, R14)."""
+def _cross_rank(cfg, stages, images, ctx, softmax):
     import synth
-    ok = True
-    first = torch.tensor([images[0]], device=dev, dtype=torch.int64)
-    firsts = [torch.zeros_like(first) for _ in range(ws)]
-    dist.all_gather(firsts, first)
-    for st in stages:
-        for key in (("y", "gom") if cfg["backward"] else ("y",)):
-            mine = st[key][:1].contiguous()
-            got = [torch.empty_like(mine) for _ in range(ws)] if rank == 0 else None
-            dist.gather(mine, got, dst=0)
-            if rank != 0:
-                continue
-            for r in range(ws):
-                n = int(firsts[r].item())
-                x, om, gy = synth.make_case(1, st["H"], st["W"], st["G"], D, st["H"], st["W"], K,
-                                            27 * st["G"], cfg["dtype"], images=[n])
-                x, om, gy = x.to(dev), om.to(dev), gy.to(dev)
-                if key == "y" and cfg.get("module"):
-                    ref = pkg.module.forward_fused(x, st["w"], st["b"], st["G"], softmax=sm)
-                elif key == "y":
-                    ref = pkg.forward(x, om, group=st["G"], softmax=sm)
-                else:
-                    ref = pkg.backward(x, om, gy, group=st["G"], softmax=sm)[1]
-                ok = ok and bool(torch.equal(ref, got[r]))
-    return {"cross_rank_bitexact": ok, "ranks": ws} if rank == 0 else None
+    pkg = ctx.pkg
+    keys = ("y", "gom") if cfg["backward"] else ("y",)
+    outputs = [st[k][:1] for st in stages for k in keys]
+
+    def recompute(n, idx):
+        st, key = stages[idx // len(keys)], keys[idx % len(keys)]
+        x, om, gy = synth.make_case(1, st["H"], st["W"], st["G"], st["D"], st["H"], st["W"], K,
+                                    27 * st["G"], cfg["dtype"], images=[n])
+        x, om = x.to(ctx.dev), om.to(ctx.dev)
+        if key == "y" and cfg.get("module"):
+            return pkg.module.forward_fused(x, st["w"], st["b"], st["G"], softmax=softmax)
+        if key == "y":
+            return pkg.forward(x, om, group=st["G"], softmax=softmax)
+        return pkg.backward(x, om, gy.to(ctx.dev), group=st["G"], softmax=softmax)[1]
+    return cross_rank_check(images[0], outputs, recompute, ctx.ws, ctx.rank, ctx.dist, ctx.dev)
 
 
-def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
+def _e2e(args, cfg, stages, ctx):
     """Same metric through the public API with pinned host buffers: every step copies the
     step's inputs host->device and its results device->host inside the timed region."""
+    torch, pkg, dev, ws = ctx.torch, ctx.pkg, ctx.dev, ctx.ws
     host = []
     h2d = d2h = 0
     for st in stages:
         h = {"x": st["x_cpu"].pin_memory(), "om": st["om_cpu"].pin_memory(),
-             "gy": st["gy_cpu"].pin_memory(), "y": torch.empty_like(st["x_cpu"]).pin_memory()}
+             "y": torch.empty_like(st["x_cpu"]).pin_memory()}
         # module: the offset_mask is computed on the device from x (weights stay resident)
         h2d += sum(h[k].numel() * h[k].element_size()
                    for k in (("x",) if cfg.get("module") else ("x", "om")))
         d2h += h["y"].numel() * h["y"].element_size()
         if cfg["backward"]:
+            h["gy"] = st["gy_cpu"].pin_memory()
             h["gx"] = torch.empty_like(st["x_cpu"]).pin_memory()
             h["gom"] = torch.empty_like(st["om_cpu"]).pin_memory()
             h2d += h["gy"].numel() * h["gy"].element_size()
@@ -616,20 +642,164 @@ def _e2e(args, cfg, stages, dev, stream, ws, pkg, torch, dist):
     pipe.run(copy_in, compute, copy_out)  # warm-up pass
     torch.cuda.synchronize(dev)
     if ws > 1:
-        dist.barrier()
+        ctx.dist.barrier()
     torch.cuda.synchronize(dev)
     evs = [pipe.run(copy_in, compute, copy_out) for _ in range(args.e2e_steps)]
     torch.cuda.synchronize(dev)
-    ms = evs[0][0].elapsed_time(evs[-1][1]) / args.e2e_steps
-    if ws > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(evs[0][0].elapsed_time(evs[-1][1]) / args.e2e_steps, ws, ctx.dist, dev)
     n_total = cfg["batch"] if cfg["shard"] else ws * len(stages[0]["x"])
     return {"value": round(n_total / (ms * 1e-3), 2), "unit": "imgs/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(ms, 3), "steps": args.e2e_steps, "chunks": nch,
             "overlap": "H2D / kernels / D2H on three streams, chunked by image"}
+
+
+def _extras(args, ctx):
+    """Forward sweeps of the default run: per-stage µs / GB/s / fraction of
+    HBM, the paper's A100 rows beside the D=32 sets, first-image oracle parity, clocks."""
+    out = []
+    for name, batch in EXTRAS:
+        cfg = dict(WORKLOADS[name], name=name)
+        if batch:
+            cfg["batch"] = batch
+        try:
+            r = measure(cfg, ctx, list(range(cfg["batch"])), None, args.warmup)
+        except Exception as e:  # a sweep must not sink the headline line
+            out.append({"workload": name, "batch": cfg["batch"], "error": repr(e)[:300]})
+            continue
+        tot_b = sum(_alg_bytes(s["x"], s["om"], cfg["backward"]) for s in r["stages"])
+        out.append({
+            "workload": name, "desc": cfg["desc"], "dtype": cfg["dtype"], "batch": cfg["batch"],
+            "imgs_per_s": round(cfg["batch"] / (r["ms_step"] * 1e-3), 1),
+            "us_per_step": round(r["ms_step"] * 1e3, 2), "steps": r["steps"],
+            "aggregate_GBs": round(tot_b / (r["ms_step"] * 1e-3) / 1e9, 1),
+            "aggregate_frac": round(tot_b / (r["ms_step"] * 1e-3) / 1e9 / _peaks()[0], 4),
+            "stages": [{k: v for k, v in row.items() if k != "checksum"} for row in r["table"]],
+            "roofline_frac_dominant": r["roofline"]["frac"], "l2": r["l2"],
+            "clocks": r["clocks"], "parity": r["parity"]})
+        for st in r["stages"]:
+            st.clear()
+        ctx.torch.cuda.empty_cache()
+    return out
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 50 for c4, else a >= 0.4 s timed region)")
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--global-batch", type=int, default=0)
+    ap.add_argument("--offsets", default="u2", choices=["u2", "zero", "u8", "smooth"])
+    ap.add_argument("--softmax", action="store_true",
+                    help="DCNv3 mode (softmax over K, NEXT-1) instead of DCNv4")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bit-reproducible grad_input (int64 fixed point, NEXT-4)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunks", type=int, default=8,
+                    help="image chunks of the host-streaming e2e pipeline (1 = no overlap)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the forward sweeps")
+    ap.add_argument("--out", default="", help="also append the JSON line to this file")
+    args = ap.parse_args(argv)
+    ws, rank, local = _dist()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args.gpus, argv)
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using the launcher's {ws} ranks",
+              file=sys.stderr)
+    cfg = dict(WORKLOADS[args.workload], name=args.workload)
+    if args.global_batch:
+        cfg["batch"] = args.global_batch
+    if args.steps is None and args.workload == "c4":
+        args.steps = 50
+    if args.warmup < 3:
+        args.warmup = 3  # contract: >= 3 untimed warm-up steps
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_06197_b200 as pkg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = Ctx(torch, dist, pkg, dev, ws, rank)
+    images = _shard(cfg["batch"], ws, rank, cfg["shard"])
+    n_img = len(images)
+    r = measure(cfg, ctx, images, args.steps, args.warmup, args.offsets, bool(args.softmax),
+                args.deterministic, verify=not args.no_verify and not (ws == 1 and args.no_cpu_baseline))
+    ms_step = r["ms_step"]
+    value = cfg["batch"] / (ms_step * 1e-3) if cfg["shard"] else ws * n_img / (ms_step * 1e-3)
+    stages = r["stages"]
+
+    e2e = _e2e(args, cfg, stages, ctx)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+    extras = None
+    if ws == 1 and not args.no_extras and args.workload == "c4":
+        for st in stages:
+            st.clear()
+        torch.cuda.empty_cache()
+        extras = _extras(args, ctx)
+    ctx.sampler.stop()
+
+    n_ours = (2 if cfg["backward"] else 1) * len(stages)
+    if cfg["backward"] and args.deterministic:
+        n_ours += 2 * len(stages)  # per-image maxima + int64 -> T conversion
+    elif cfg["backward"] and cfg["dtype"] != "f32":
+        n_ours += len(stages)  # fp32 -> half grad_input conversion
+    Ds = sorted({d for *_, d in cfg["stages"]})
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "imgs/s", "n_gpus": ws,
+        "steps": r["steps"], "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong" if cfg["shard"] else "weak",
+        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": {"workload": cfg["name"], "desc": cfg["desc"], "global_batch": cfg["batch"],
+                   "per_gpu_batch": n_img, "stages": [shape_name(*s) for s in cfg["stages"]],
+                   "D": Ds[0] if len(Ds) == 1 else Ds, "kernel": "3x3 s1 p1 d1",
+                   "offset_scale": 1.0, "offsets": args.offsets,
+                   "operator": "DCNv3 (softmax over K)" if args.softmax else "DCNv4",
+                   "grad_input": ("deterministic int64 fixed point" if args.deterministic
+                                  else "fp32 atomics") if cfg["backward"] else None,
+                   "parallelism": f"batch-sharded dp{ws}" if cfg["shard"] else f"replicas x{ws}",
+                   "l2": r["l2"]},
+        "roofline": r["roofline"],
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": n_ours * r["steps"],
+        "gpu_launch_detail": f"per step: {len(stages)} "
+                             + ("module_fwd_kernel" if cfg.get("module") else "fwd33_kernel")
+                             + (f" + {len(stages)} bwd33_kernel + {len(stages)} accumulator "
+                                f"zero-fill (cudaMemsetAsync)" if cfg["backward"] else "")
+                             + (f" + {len(stages)} det_scale_kernel + {len(stages)} det_convert_kernel"
+                                if cfg["backward"] and args.deterministic else
+                                f" + {len(stages)} convert_kernel" if cfg["backward"] and cfg["dtype"] != "f32"
+                                else ""),
+        "clocks": r["clocks"],
+        "stages": r["table"],
+        "parity": r["parity"],
+        "wall_s_timed_region": r["wall_s"],
+        "forward_sweeps": extras,
+    }
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(s + "\n")
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import concurrent.futures as cf
+import hashlib
 import os
 import subprocess
 import sys
@@ -17,11 +18,23 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-Xptxas", "-v", "-Xcompiler", "-Wall"]
 
 
-def _deps():
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    for h in ("dcnv4.h", "msda.h", "dcnv4_module.h"):
-        files.append(os.path.join(os.path.dirname(HERE), "include", h))
-    return max(os.path.getmtime(f) for f in files)
+def _source_hash() -> str:
+    """sha256 over every CUDA source/header, the ABI headers and the compiler command: the
+    library is rebuilt whenever any of them differs from what the in-tree .so was built
+    from (not by mtime, so a stale prebuilt binary never stands in for HEAD)."""
+    h = hashlib.sha256()
+    files = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC))
+    for name in ("dcnv4.h", "msda.h", "dcnv4_module.h"):
+        files.append(os.path.join(os.path.dirname(HERE), "include", name))
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join([NVCC, *ARCH, *FLAGS, *SOURCES]).encode())
+    return h.hexdigest()
+
+
+STAMP = os.path.join(BUILD, "libdcnv4.sha256")
 
 
 def _compile(src: str) -> str:
@@ -37,8 +50,11 @@ def _compile(src: str) -> str:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps():
-        return LIB
+    digest = _source_hash()
+    if not force and os.path.exists(LIB) and os.path.exists(STAMP):
+        with open(STAMP) as f:
+            if f.read().strip() == digest:
+                return LIB
     os.makedirs(BUILD, exist_ok=True)
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(_compile, SOURCES))
@@ -46,6 +62,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(digest + "\n")
     if verbose:
         print(f"built {LIB}", file=sys.stderr)
     return LIB

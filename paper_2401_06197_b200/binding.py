@@ -149,6 +149,38 @@ def _check_tensors(*ts):
         raise ValueError(f"unsupported dtype {ts[0].dtype}")
 
 
+def _check_buffer(t: torch.Tensor, shape, like: torch.Tensor, name: str):
+    """A caller-supplied output buffer: exact shape, the inputs' dtype and device,
+    contiguous (the kernels and TMA maps size everything from the params)."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} is {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.dtype != like.dtype:
+        raise ValueError(f"{name} has dtype {t.dtype}, expected {like.dtype}")
+    if t.device != like.device:
+        raise ValueError(f"{name} is on {t.device}, expected {like.device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _workspace(workspace: Optional[torch.Tensor], need: int, like: torch.Tensor):
+    """A caller-supplied scratch buffer (any dtype, >= need bytes, same device,
+    contiguous), or a fresh one."""
+    if not need:
+        return None
+    if workspace is None:
+        return torch.empty(need, dtype=torch.uint8, device=like.device)
+    if workspace.device != like.device:
+        raise ValueError(f"workspace is on {workspace.device}, expected {like.device}")
+    if not workspace.is_contiguous():
+        raise ValueError("workspace must be contiguous")
+    if workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"workspace has {workspace.numel() * workspace.element_size()} bytes, "
+                         f"{need} required")
+    return workspace
+
+
 def forward(x: torch.Tensor, offset_mask: torch.Tensor, group: int, kernel_size=3, stride=1,
             pad=1, dilation=1, offset_scale=1.0, softmax=False,
             out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -159,6 +191,7 @@ def forward(x: torch.Tensor, offset_mask: torch.Tensor, group: int, kernel_size=
     Ho, Wo = output_size(p)
     if out is None:
         out = torch.empty((x.shape[0], Ho, Wo, x.shape[3]), dtype=x.dtype, device=x.device)
+    _check_buffer(out, (x.shape[0], Ho, Wo, x.shape[3]), x, "out")
     with torch.cuda.device(x.device):
         _check(lib().dcnv4_forward(ctypes.byref(p), DTYPE_CODE[x.dtype], _ptr(x),
                                    _ptr(offset_mask), _ptr(out), ctypes.c_void_p(_stream_ptr(x))))
@@ -179,13 +212,16 @@ def backward(x: torch.Tensor, offset_mask: torch.Tensor, grad_output: torch.Tens
     _check_tensors(x, offset_mask, grad_output)
     p = _params_for(x, offset_mask, group, kernel_size, stride, pad, dilation, offset_scale,
                     softmax, deterministic)
+    Ho, Wo = output_size(p)
+    _check_buffer(grad_output, (x.shape[0], Ho, Wo, x.shape[3]), x, "grad_output")
     if grad_input is None:
         grad_input = torch.empty_like(x)
     if grad_offset_mask is None:
         grad_offset_mask = torch.empty_like(offset_mask)
+    _check_buffer(grad_input, x.shape, x, "grad_input")
+    _check_buffer(grad_offset_mask, offset_mask.shape, x, "grad_offset_mask")
     need = workspace_bytes(p, x.dtype)
-    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
-        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    workspace = _workspace(workspace, need, x)
     with torch.cuda.device(x.device):
         _check(lib().dcnv4_backward(ctypes.byref(p), DTYPE_CODE[x.dtype], _ptr(x),
                                     _ptr(offset_mask), _ptr(grad_output), _ptr(grad_input),

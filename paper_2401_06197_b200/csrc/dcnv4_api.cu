@@ -14,6 +14,7 @@
 #include "../../include/dcnv4.h"
 #include "dcnv4_kernels.cuh"
 #include "dcnv4_launch.h"
+#include "ablation.h"
 
 namespace {
 
@@ -181,31 +182,27 @@ TileChoice choose_tile_search(const dcnv4_params* p, int b, int nch, int cpl, in
                               int64_t Wo, bool halo);
 
 // The tile search costs tens of microseconds of host time per call and depends only on
-// the geometry, the chunking and the DCNV4_TILE override: memoised per host thread.
+// the geometry and the chunking (the DCNV4_TILE ablation is fixed at first use): memoised
+// per host thread.
 TileChoice choose_tile(const dcnv4_params* p, int b, int nch, int cpl, int64_t Ho, int64_t Wo,
                        bool halo) {
   struct Memo {
     dcnv4_params p;
     int b, nch, cpl, halo;
-    char env[32];
     TileChoice tc;
   };
   thread_local Memo memo[32];
   thread_local int memo_n = 0, memo_next = 0;
-  const char* env = getenv("DCNV4_TILE");
-  char ebuf[32] = {0};
-  if (env) snprintf(ebuf, sizeof(ebuf), "%s", env);
   for (int i = 0; i < memo_n; ++i) {
     const Memo& m = memo[i];
     if (m.b == b && m.nch == nch && m.cpl == cpl && m.halo == (int)halo &&
-        memcmp(&m.p, p, sizeof(dcnv4_params)) == 0 && memcmp(m.env, ebuf, sizeof(ebuf)) == 0)
+        memcmp(&m.p, p, sizeof(dcnv4_params)) == 0)
       return m.tc;
   }
   const TileChoice tc = choose_tile_search(p, b, nch, cpl, Ho, Wo, halo);
   Memo& m = memo[memo_next];
   memcpy(&m.p, p, sizeof(dcnv4_params));
   m.b = b; m.nch = nch; m.cpl = cpl; m.halo = (int)halo;
-  memcpy(m.env, ebuf, sizeof(ebuf));
   m.tc = tc;
   memo_next = (memo_next + 1) % 32;
   memo_n = memo_n < 32 ? memo_n + 1 : 32;
@@ -221,7 +218,7 @@ TileChoice choose_tile_search(const dcnv4_params* p, int b, int nch, int cpl, in
   const double kappa = 3.0;     // L2->L1 byte vs L1-hit byte
   TileChoice best = {1, 1, G, -1};
   double best_cost = 1e300;
-  const char* env = getenv("DCNV4_TILE");
+  const char* env = dcnv4::ablation(dcnv4::kAblTile);
   int fth = 0, ftw = 0, fgc = 0;
   if (env && *env) sscanf(env, "%d,%d,%d", &fth, &ftw, &fgc);
   const int cand[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 20, 24, 25, 28, 32, 40, 50, 56, 64};
@@ -316,7 +313,7 @@ bool encode_nhwc_map(int dtype, const void* ptr, int64_t N, int64_t Hh, int64_t 
 // keeps the global-gather kernel.  `x` may be NULL (planning only, lc->halo stays false).
 bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const void* x,
                 dcnv4::Launch* lc, dcnv4::Geo* g) {
-  const char* path = getenv("DCNV4_FWD_PATH");
+  const char* path = dcnv4::ablation(dcnv4::kAblFwdPath);
   if (path && path[0] == 'g') return false;
   if (p->kernel_h != 3 || p->kernel_w != 3 || p->stride_h != 1 || p->stride_w != 1 ||
       p->dilation_h != 1 || p->dilation_w != 1)
@@ -332,7 +329,7 @@ bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   // (profiles/r01_fwd_th_sweep.jsonl)
   int TH = std::max(1, 128 / per_row);
   if (TH < 1) return false;
-  const char* th_env = getenv("DCNV4_FWD33_TH");
+  const char* th_env = dcnv4::ablation(dcnv4::kAblFwd33TH);
   if (th_env && *th_env) TH = std::max(1, std::min(TH, atoi(th_env)));
   if (TH > Ho) TH = (int)Ho;
   const int K = 9;
@@ -342,6 +339,9 @@ bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   for (int u : {8, 4})
     if ((S * b) % u == 0 && segB_raw % u == 0) { unit = u; break; }
   if (!unit) return false;
+  // the kernels form a tile pixel's offset_mask source offset (row * Wo*S*b + col * S*b)
+  // in 32-bit unsigned arithmetic
+  if ((long long)(TH + 1) * std::max<int64_t>(Wo, 8) * S * b >= (1LL << 32)) return false;
   int seg_bytes = (segB_raw + 15) & ~15;
   if ((seg_bytes / 16) % 2 == 0) seg_bytes += 16;
   const int HH = TH + 6, HWc = 14;
@@ -388,7 +388,7 @@ bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
 // per SM overlap each other's loads).  Needs x and gy pointers for the TMA maps.
 bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const void* x,
                 const void* gy, dcnv4::Launch* lc, dcnv4::Geo* g) {
-  const char* path = getenv("DCNV4_BWD_PATH");
+  const char* path = dcnv4::ablation(dcnv4::kAblBwdPath);
   if (path && path[0] == 'g') return false;
   if (p->kernel_h != 3 || p->kernel_w != 3 || p->stride_h != 1 || p->stride_w != 1 ||
       p->dilation_h != 1 || p->dilation_w != 1)
@@ -402,7 +402,7 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   const int per_row = 8 * GC * L;
   int TH = 256 / per_row;
   if (TH < 1) return false;
-  const char* th_env = getenv("DCNV4_BWD33_TH");
+  const char* th_env = dcnv4::ablation(dcnv4::kAblBwd33TH);
   if (th_env && *th_env) TH = std::max(1, std::min(TH, atoi(th_env)));
   if (TH > Ho) TH = (int)Ho;
   const int K = 9;
@@ -412,6 +412,9 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   for (int u : {8, 4})
     if ((S * b) % u == 0 && segB_raw % u == 0) { unit = u; break; }
   if (!unit) return false;
+  // the kernels form a tile pixel's offset_mask source offset (row * Wo*S*b + col * S*b)
+  // in 32-bit unsigned arithmetic
+  if ((long long)(TH + 1) * std::max<int64_t>(Wo, 8) * S * b >= (1LL << 32)) return false;
   int seg_bytes = (segB_raw + 15) & ~15;
   if ((seg_bytes / 16) % 2 == 0) seg_bytes += 16;
   const int npix = TH * 8, HH = TH + 6, NT = HH * 14;
@@ -479,7 +482,7 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
     profile(8, 14, px_);
     int idx[200];
     for (int i = 0; i < NT; ++i) idx[i] = i;
-    const char* ord = getenv("DCNV4_P4ORDER");
+    const char* ord = dcnv4::ablation(dcnv4::kAblP4Order);
     if (!(ord && *ord == '0'))
       std::stable_sort(idx, idx + NT, [&](int a, int b2) {
         return py_[a / 14] * px_[a % 14] > py_[b2 / 14] * px_[b2 % 14];
@@ -508,7 +511,7 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
   const int b = elem_size(dtype);
   const int nch = p->D * b / 16;
   int cpl = default_cpl(nch, pass);
-  const char* env = getenv(pass == 0 ? "DCNV4_FWD_CPL" : "DCNV4_BWD_CPL");
+  const char* env = dcnv4::ablation(pass == 0 ? dcnv4::kAblFwdCpl : dcnv4::kAblBwdCpl);
   if (env && *env) {
     int v = atoi(env);
     if (cpl_supported(nch, v)) cpl = v;
@@ -555,8 +558,7 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
   if (pass == 0) plan_fwd33(p, dtype, Ho, Wo, x, lc, g);
   else plan_bwd33(p, dtype, Ho, Wo, x, gy, lc, g);
   g->tiles_total = (int)lc->ctas;
-  const char* np = getenv("DCNV4_NONPERSISTENT");
-  lc->persistent = !(np && *np == '1');
+  lc->persistent = dcnv4::ablation(dcnv4::kAblNonPersistent)[0] != '1';
   lc->det = pass == 1 && p->deterministic;
   {  // ceil(log2(Ho*Wo*K)): bound on the contributions one input element receives
     const long long cnt = (long long)Ho * Wo * K;

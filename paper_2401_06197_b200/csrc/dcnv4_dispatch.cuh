@@ -152,13 +152,17 @@ static inline unsigned flat_blocks(long long n) {
                                      cudaStream_t stream) {                                     \
     if (N <= 0) return cudaSuccess;                                                             \
     const long long chunks = (long long)npix * C / Elem<T>::E;                                 \
-    long long per = (chunks + 255) / 256;                                                      \
-    const long long want = (148LL * 8 + N - 1) / N;                                            \
-    if (per > want) per = want;                                                                 \
-    dim3 grid((unsigned)(per < 1 ? 1 : per), (unsigned)N);                                      \
-    det_scale_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(gy),                   \
-                                                  static_cast<const T*>(om), chunks, npix, S, G, K, \
-                                                  softmax, mx);                                 \
+    /* images on grid.y, at most 65535 per launch */                                         \
+    for (long long n0 = 0; n0 < N; n0 += 65535) {                                               \
+      const long long nb = N - n0 < 65535 ? N - n0 : 65535;                                     \
+      long long per = (chunks + 255) / 256;                                                     \
+      const long long want = (148LL * 8 + nb - 1) / nb;                                         \
+      if (per > want) per = want;                                                               \
+      dim3 grid((unsigned)(per < 1 ? 1 : per), (unsigned)nb);                                   \
+      det_scale_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T*>(gy),                  \
+                                                    static_cast<const T*>(om), chunks, npix, S, G, \
+                                                    K, softmax, mx, n0);                        \
+    }                                                                                           \
     return cudaGetLastError();                                                                  \
   }                                                                                             \
   cudaError_t launch_detconv_##SUFFIX(const long long* src, const unsigned* mx, int lc,         \

@@ -1458,15 +1458,15 @@ __global__ void __launch_bounds__(256) convert_kernel(const float* __restrict__ 
 
 // Deterministic mode, pass 1: per-image maxima {max|gy|, max|m|} as float bits
 // (non-negative floats order as unsigned integers; NaN sorts above +inf).  grid =
-// (blocks per image, N); mx must be zeroed.  softmax: the mask bound is 1 (softmax
+// (blocks per image, images of this launch), image n = n0 + blockIdx.y; mx must be zeroed.  softmax: the mask bound is 1 (softmax
 // outputs), unless a logit is non-finite.
 template <typename T>
 __global__ void __launch_bounds__(256) det_scale_kernel(const T* __restrict__ gy,
                                                         const T* __restrict__ om, long long gy_chunks,
                                                         int npix, int S, int G, int K, int softmax,
-                                                        unsigned* __restrict__ mx) {
+                                                        unsigned* __restrict__ mx, long long n0) {
   constexpr int E = Elem<T>::E;
-  const int n = blockIdx.y;
+  const long long n = n0 + blockIdx.y;
   const int nt = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned vg = 0u, vm = 0u;

@@ -21,6 +21,7 @@
 #include "../../include/dcnv4_module.h"
 #include "dcnv4_kernels.cuh"
 #include "sm100_tc.cuh"
+#include "ablation.h"
 
 namespace oml {
 
@@ -366,7 +367,7 @@ cudaError_t launch_module(const CUtensorMap& hm, const CUtensorMap& am, const CU
   const int by_smem = (int)((228 * 1024) / (smem + 1024));
   if (by_smem < per_sm) per_sm = by_smem;
   if ((int)(512 / g.tmem_cols) < per_sm) per_sm = (int)(512 / g.tmem_cols);
-  if (const char* f = getenv("DCNV4_MODULE_PER_SM")) per_sm = atoi(f);  // ablation only
+  if (dcnv4::ablation_set(dcnv4::kAblModulePerSm)) per_sm = atoi(dcnv4::ablation(dcnv4::kAblModulePerSm));  // ablation only
   if (per_sm < 1) per_sm = 1;
   const long long cap = (long long)sms * per_sm;
   const unsigned grid = (unsigned)(g.tiles_total < cap ? g.tiles_total : cap);
@@ -436,18 +437,25 @@ int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* i
   const int JB = GC * 27;
   g.BN = (JB + 15) / 16 * 16;
   g.kb = (int)((C + BK - 1) / BK);
-  // operand ring: one stage (72 KB of shared memory -> 3 CTAs/SM, other CTAs hide the
-  // k-block loads) up to 4 k blocks (C <= 256); two stages beyond, where a tile's 8
-  // sequential k-block rounds dominate (c2 C=512: 28.7 vs 32.6 us; C=128: 46.9 vs 53.2 us,
-  // profiles/r01b_module_stages_ab.txt).  DCNV4_MODULE_STAGES=1|2 overrides (ablation).
-  g.stages = g.kb <= 4 ? 1 : 2;
-  if (const char* se = getenv("DCNV4_MODULE_STAGES")) {
-    const int v = atoi(se);
-    if (v == 1 || v == 2) g.stages = v <= g.kb ? v : g.stages;
-  }
   g.tiles_h = (int)((p->H + 15) / 16);
   g.tiles_w = (int)((p->W + 7) / 8);
   g.gblocks = p->G / GC;
+  // operand ring: one stage (72 KB of shared memory -> 3 CTAs/SM, other CTAs hide the
+  // k-block loads) up to 4 k blocks (C <= 256).  Beyond that a tile's 8 sequential k-block
+  // rounds dominate and two stages pay -- but only when there are enough tiles for every
+  // SM to hold two (c2 C=512, 512 tiles: 28.7 vs 32.6 us); with fewer tiles than that
+  // each CTA runs ~one tile and the extra shared memory only costs (c3 batch 1 C=512,
+  // 80 tiles: one stage 44.96 vs two 47.14 us; profiles/r01b_module_stages_ab.txt).
+  // DCNV4_MODULE_STAGES=1|2 overrides (ablation).
+  {
+    const long long ntiles = p->N * g.tiles_h * g.tiles_w * (long long)g.gblocks;
+    g.stages = (g.kb > 4 && ntiles >= 2LL * num_sms()) ? 2 : 1;
+  }
+  if (dcnv4::ablation_set(dcnv4::kAblModuleStages)) {
+    const char* se = dcnv4::ablation(dcnv4::kAblModuleStages);
+    const int v = atoi(se);
+    if (v == 1 || v == 2) g.stages = v <= g.kb ? v : g.stages;
+  }
   const long long tiles = p->N * g.tiles_h * g.tiles_w * (long long)g.gblocks;
   if (tiles >= (1LL << 31)) return fail(DCNV4_ERR_SHAPE, "too many tiles");
   g.tiles_total = (int)tiles;

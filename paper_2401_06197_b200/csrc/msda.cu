@@ -22,6 +22,7 @@
 #include <stdlib.h>
 
 #include "../../include/msda.h"
+#include "ablation.h"
 #include "dcnv4_kernels.cuh"
 
 void dcnv4_internal_set_error(const char* msg);  // dcnv4_api.cu (not exported)
@@ -458,7 +459,7 @@ MGeo make_geo(const msda_params* p, long long S) {
   g.items = p->N * p->Lq * p->M;
   g.chunk = 0;
   g.nimg = p->N;
-  const char* ord = getenv("MSDA_ORDER");
+  const char* ord = dcnv4::ablation(dcnv4::kAblMsdaOrder);
   g.qfast = (ord && ord[0] == 'q') ? 1 : 0;  // ablation only: measured no better
   return g;
 }
@@ -466,7 +467,7 @@ MGeo make_geo(const msda_params* p, long long S) {
 // chunks per lane: whole 128-B corner lines per item when possible (env MSDA_CPL overrides)
 int pick_cpl(int nch) {
   int cpl = nch <= 8 ? 1 : nch / 8;
-  const char* env = getenv("MSDA_CPL");
+  const char* env = dcnv4::ablation(dcnv4::kAblMsdaCpl);
   if (env && *env) {
     const int v = atoi(env);
     if (v >= 1 && v <= nch && (v & (v - 1)) == 0 && nch / v <= 32) cpl = v;
@@ -482,7 +483,7 @@ int pick_cpl(int nch) {
 // restores the capped launch (ablation).
 unsigned grid_for(long long threads) {
   long long b = (threads + 255) / 256;
-  const char* env = getenv("MSDA_GRID_CAP");
+  const char* env = dcnv4::ablation(dcnv4::kAblMsdaGridCap);
   const long long cap = (env && *env == '1') ? 148LL * 8 * 4 : 0x7fffffffLL;
   return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
 }
@@ -493,7 +494,7 @@ unsigned grid_for(long long threads) {
 // launch (grid_for).
 template <typename K, typename... A>
 cudaError_t launch_sched(K k, MGeo g, long long thr, cudaStream_t st, A... args) {
-  const char* env = getenv("MSDA_SCHED");
+  const char* env = dcnv4::ablation(dcnv4::kAblMsdaSched);
   unsigned grid;
   g.chunk = 0;
   g.nimg = 1;
@@ -521,7 +522,7 @@ cudaError_t launch_fwd(const MGeo& g, int nch, int cpl, const void* v, const voi
   // vectorised sample records (L*P = 16, 16-B aligned loc / attn): opt-in, MSDA_VEC=1 --
   // measured slower than scalar loads (f32 fwd 757 -> 965 us: 80-90 registers)
   const bool v16 = g.L * g.P == 16 && ((reinterpret_cast<uintptr_t>(lo) | reinterpret_cast<uintptr_t>(at)) & 15) == 0 &&
-                   (getenv("MSDA_VEC") && *getenv("MSDA_VEC") == '1');
+                   (*dcnv4::ablation(dcnv4::kAblMsdaVec) == '1');
   const T* vp = static_cast<const T*>(v);
   const T* lp = static_cast<const T*>(lo);
   const T* ap = static_cast<const T*>(at);
@@ -550,7 +551,7 @@ cudaError_t launch_bwd(const MGeo& g, int nch, int cpl, const void* v, const voi
   const T* gp = static_cast<const T*>(go);
   T* glp = static_cast<T*>(gl);
   T* gap = static_cast<T*>(ga);
-  if (sizeof(T) == 2 && !(getenv("MSDA_BWD8") && *getenv("MSDA_BWD8") == '0')) {
+  if (sizeof(T) == 2 && *dcnv4::ablation(dcnv4::kAblMsdaBwd8) != '0') {
     const long long thr8 = g.items * (g.D / 4);
     switch (g.D / 4) {
       case 4: return launch_sched(msda_bwd8_kernel<T, 4>, g, thr8, st, vp, lp, ap, gp, gv, glp, gap);
@@ -562,7 +563,7 @@ cudaError_t launch_bwd(const MGeo& g, int nch, int cpl, const void* v, const voi
   }
   const long long thr = g.items * (nch / cpl);
   const bool v16 = g.L * g.P == 16 && ((reinterpret_cast<uintptr_t>(lo) | reinterpret_cast<uintptr_t>(at)) & 15) == 0 &&
-                   (getenv("MSDA_VEC") && *getenv("MSDA_VEC") == '1');
+                   (*dcnv4::ablation(dcnv4::kAblMsdaVec) == '1');
 #define MSDA_BWD(NC, CP)                                                                          \
   case NC * 100 + CP:                                                                             \
     return v16 ? launch_sched(msda_bwd_kernel<T, NC, CP, 16>, g, thr, st, vp, lp, ap, gp, gv, glp, gap) \

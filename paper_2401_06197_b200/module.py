@@ -14,7 +14,7 @@ from typing import Optional
 
 import torch
 
-from .binding import DTYPE_CODE, _check, _check_tensors, _ptr, _stream_ptr, lib, make_params
+from .binding import DTYPE_CODE, _check, _check_buffer, _check_tensors, _ptr, _stream_ptr, lib, make_params
 from .binding import forward as dcnv4_forward
 from .binding import output_size
 
@@ -36,6 +36,15 @@ def _lib():
     return L
 
 
+def _check_linear(weight: torch.Tensor, bias: Optional[torch.Tensor], group: int, C: int, K: int):
+    """weight [3*G*K, C] (nn.Linear layout), bias [3*G*K] (R21)."""
+    J = 3 * group * K
+    if tuple(weight.shape) != (J, C):
+        raise ValueError(f"weight is {tuple(weight.shape)}, expected [3*G*K, C] = [{J}, {C}]")
+    if bias is not None and tuple(bias.shape) != (J,):
+        raise ValueError(f"bias is {tuple(bias.shape)}, expected [{J}]")
+
+
 def om_stride_for(G: int, K: int = 9, multiple: int = 8) -> int:
     """Padded offset_mask row length: 3*G*K rounded up to `multiple` channels (16-B rows)."""
     return -(-3 * G * K // multiple) * multiple
@@ -51,6 +60,9 @@ def offset_mask_linear(x: torch.Tensor, weight: torch.Tensor, bias: Optional[tor
     N, H, W, C = x.shape
     kh, kw = (kernel_size, kernel_size) if isinstance(kernel_size, int) else kernel_size
     S = om_stride if om_stride else om_stride_for(group, kh * kw)
+    if C % group:
+        raise ValueError(f"C = {C} is not divisible by group = {group}")
+    _check_linear(weight, bias, group, C, kh * kw)
     p = make_params(N, H, W, group, C // group, (kh, kw), 1, ((kh - 1) // 2, (kw - 1) // 2), 1,
                     1.0, S)
     Ho, Wo = output_size(p)
@@ -58,6 +70,7 @@ def offset_mask_linear(x: torch.Tensor, weight: torch.Tensor, bias: Optional[tor
         raise ValueError("offset_mask_linear needs a 'same' geometry (odd kernel)")
     if out is None:
         out = torch.empty((N, H, W, S), dtype=x.dtype, device=x.device)
+    _check_buffer(out, (N, H, W, S), x, "out")
     with torch.cuda.device(x.device):
         _check(_lib().dcnv4_offset_mask_linear(ctypes.byref(p), DTYPE_CODE[x.dtype], C, _ptr(x),
                                                _ptr(weight), _ptr(bias), _ptr(out),
@@ -84,9 +97,11 @@ def forward_fused(x: torch.Tensor, weight: torch.Tensor, bias: Optional[torch.Te
     N, H, W, C = x.shape
     if C % group:
         raise ValueError(f"C = {C} is not divisible by group = {group}")
+    _check_linear(weight, bias, group, C, 9)
     p = make_params(N, H, W, group, C // group, 3, 1, 1, 1, offset_scale, 0, softmax)
     if out is None:
         out = torch.empty_like(x)
+    _check_buffer(out, x.shape, x, "out")
     with torch.cuda.device(x.device):
         _check(_lib().dcnv4_module_forward(ctypes.byref(p), DTYPE_CODE[x.dtype], _ptr(x), _ptr(weight),
                                            _ptr(bias), _ptr(out), ctypes.c_void_p(_stream_ptr(x))))

@@ -13,7 +13,7 @@ from typing import Optional, Sequence, Tuple
 
 import torch
 
-from .binding import DTYPE_CODE, _check, _check_tensors, _ptr, _stream_ptr, lib
+from .binding import DTYPE_CODE, _check, _check_buffer, _check_tensors, _ptr, _stream_ptr, _workspace, lib
 
 MAX_LEVELS = 8
 
@@ -86,6 +86,7 @@ def forward(value, loc, attn, shapes, out: Optional[torch.Tensor] = None) -> tor
     p = _params_for(value, loc, attn, shapes)
     if out is None:
         out = torch.empty((p.N, p.Lq, p.M, p.D), dtype=value.dtype, device=value.device)
+    _check_buffer(out, (p.N, p.Lq, p.M, p.D), value, "out")
     with torch.cuda.device(value.device):
         _check(_lib().msda_forward(ctypes.byref(p), DTYPE_CODE[value.dtype], _ptr(value), _ptr(loc),
                                    _ptr(attn), _ptr(out), ctypes.c_void_p(_stream_ptr(value))))
@@ -100,9 +101,12 @@ def backward(value, loc, attn, grad_out, shapes, grad_value=None, grad_loc=None,
     grad_value = torch.empty_like(value) if grad_value is None else grad_value
     grad_loc = torch.empty_like(loc) if grad_loc is None else grad_loc
     grad_attn = torch.empty_like(attn) if grad_attn is None else grad_attn
+    _check_buffer(grad_out, (p.N, p.Lq, p.M, p.D), value, "grad_out")
+    _check_buffer(grad_value, value.shape, value, "grad_value")
+    _check_buffer(grad_loc, loc.shape, value, "grad_loc")
+    _check_buffer(grad_attn, attn.shape, value, "grad_attn")
     need = workspace_bytes(p, value.dtype)
-    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
-        workspace = torch.empty(need, dtype=torch.uint8, device=value.device)
+    workspace = _workspace(workspace, need, value)
     with torch.cuda.device(value.device):
         _check(_lib().msda_backward(ctypes.byref(p), DTYPE_CODE[value.dtype], _ptr(value), _ptr(loc),
                                     _ptr(attn), _ptr(grad_out), _ptr(grad_value), _ptr(grad_loc),

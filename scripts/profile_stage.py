@@ -26,10 +26,10 @@ def main():
     ap.add_argument("--offsets", default="u2")
     args = ap.parse_args()
     cfg = bench.WORKLOADS[args.workload]
-    H, W, G = cfg["stages"][args.stage]
+    H, W, G, D = cfg["stages"][args.stage]
     N = args.batch or cfg["batch"]
     dev = torch.device("cuda:0")
-    x, om, gy = synth.make_case(N, H, W, G, 16, H, W, 9, 27 * G, cfg["dtype"],
+    x, om, gy = synth.make_case(N, H, W, G, D, H, W, 9, 27 * G, cfg["dtype"],
                                 offsets=args.offsets)
     x, om, gy = x.to(dev), om.to(dev), gy.to(dev)
     y = torch.empty_like(x)
@@ -40,8 +40,8 @@ def main():
         if cfg["backward"] and not args.fwd_only:
             pkg.backward(x, om, gy, group=G, grad_input=gx, grad_offset_mask=gom)
     torch.cuda.synchronize()
-    print("launch info fwd", pkg.launch_info(pkg.make_params(N, H, W, G, 16), x.dtype))
-    print("launch info bwd", pkg.launch_info(pkg.make_params(N, H, W, G, 16), x.dtype, True))
+    print("launch info fwd", pkg.launch_info(pkg.make_params(N, H, W, G, D), x.dtype))
+    print("launch info bwd", pkg.launch_info(pkg.make_params(N, H, W, G, D), x.dtype, True))
 
 
 if __name__ == "__main__":

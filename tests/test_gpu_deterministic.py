@@ -33,9 +33,30 @@ def _inputs(N, H, W, G, dtype, offsets="u2", images=None):
     return x.to(dev), om.to(dev), gy.to(dev)
 
 
+def _det_backward_with_switch(env: dict, N, H, W, G, dtype, offsets, reps=1):
+    """grad_input of `reps` deterministic backward calls in a fresh process whose
+    environment holds an ablation switch (the library reads its switches once, at first
+    use: csrc/ablation.h), on the same seeded inputs as _inputs()."""
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "gx.pt")
+        code = ("import torch, sys; sys.path.insert(0, %r)\n"
+                "from tests.test_gpu_deterministic import _inputs\n"
+                "import paper_2401_06197_b200 as pkg\n"
+                "x, om, gy = _inputs(%d, %d, %d, %d, %r, %r)\n"
+                "r = [pkg.backward(x, om, gy, group=%d, deterministic=True)[0].cpu() for _ in range(%d)]\n"
+                "torch.save(r, %r)\n") % (root, N, H, W, G, dtype, offsets, G, reps, out)
+        subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env),
+                       check=True, timeout=300)
+        return torch.load(out)
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("offsets", ["u2", "u8"])
-def test_bit_identical_runs_grids_and_splits(dtype, offsets, monkeypatch):
+def test_bit_identical_runs_grids_and_splits(dtype, offsets):
     N, H, W, G = 6, 28, 28, 8
     x, om, gy = _inputs(N, H, W, G, dtype, offsets)
     ref, gom_ref = pkg.backward(x, om, gy, group=G, deterministic=True)
@@ -43,17 +64,12 @@ def test_bit_identical_runs_grids_and_splits(dtype, offsets, monkeypatch):
         gx, gom = pkg.backward(x, om, gy, group=G, deterministic=True)
         assert torch.equal(gx, ref) and torch.equal(gom, gom_ref)
     # a different CTA -> tile assignment (one CTA per tile instead of a persistent grid)
-    monkeypatch.setenv("DCNV4_NONPERSISTENT", "1")
-    gx, _ = pkg.backward(x, om, gy, group=G, deterministic=True)
-    assert torch.equal(gx, ref)
-    monkeypatch.delenv("DCNV4_NONPERSISTENT")
+    (gx,) = _det_backward_with_switch({"DCNV4_NONPERSISTENT": "1"}, N, H, W, G, dtype, offsets)
+    assert torch.equal(gx, ref.cpu())
     # the global-gather kernel agrees with the TMA-halo kernel only within tolerance, but
     # is itself reproducible
-    monkeypatch.setenv("DCNV4_BWD_PATH", "g")
-    a, _ = pkg.backward(x, om, gy, group=G, deterministic=True)
-    b, _ = pkg.backward(x, om, gy, group=G, deterministic=True)
+    a, b = _det_backward_with_switch({"DCNV4_BWD_PATH": "g"}, N, H, W, G, dtype, offsets, reps=2)
     assert torch.equal(a, b)
-    monkeypatch.delenv("DCNV4_BWD_PATH")
     # batch split: per-image scale, so a sub-batch reproduces its slice bit for bit
     for lo, hi in ((0, 1), (2, 5), (5, 6)):
         part, _ = pkg.backward(x[lo:hi].contiguous(), om[lo:hi].contiguous(),
