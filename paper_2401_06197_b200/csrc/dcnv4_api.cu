@@ -428,14 +428,14 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   o = up(o + gy_box, 128);
   const int o_om = (int)o;
   o = up(o + (size_t)npix * seg_bytes, 16);
-  const int o_gom = (int)o;
-  o = up(o + (size_t)npix * GC * 3 * K * 4, 16);
+  const int o_gom = -1;  // grad_offset_mask goes straight from registers to memory
   const int o_cnt = (int)o;
   o = up(o + ((size_t)GC * NT + 1) * 4, 16);
   const int o_slot = (int)o;
   o = up(o + (size_t)GC * NT * 4, 16);  // fill pointers
   const int o_ent = (int)o;
-  o = up(o + ((size_t)GC * npix * 36 + (size_t)GC * NT) * 8, 16);  // + one pad slot per bin
+  // bin entries: 8 B {a, src} for fp32, 4 B {a in T, src} for half (+ one pad slot per bin)
+  o = up(o + ((size_t)GC * npix * 36 + (size_t)GC * NT) * (b == 4 ? 8 : 4), 16);
   const int o_wsum = (int)o;
   o = up(o + 33 * 4, 16);
   const int o_bar = (int)o;

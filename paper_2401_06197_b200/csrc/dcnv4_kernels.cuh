@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace dcnv4 {
 
 // Geometry handed to every kernel by value (validated on the host; per-image element
@@ -86,6 +88,8 @@ struct Elem<float> {
                       __float_as_uint(v[3]));
   }
   __device__ __forceinline__ static float from_f32(float v) { return v; }
+  __device__ __forceinline__ static unsigned short bits(float) { return 0; }  // unused (8-B entries)
+  __device__ __forceinline__ static float from_bits(unsigned short) { return 0.f; }
 };
 template <>
 struct Elem<__half> {
@@ -110,6 +114,8 @@ struct Elem<__half> {
     return make_uint4(w[0], w[1], w[2], w[3]);
   }
   __device__ __forceinline__ static __half from_f32(float v) { return __float2half_rn(v); }
+  __device__ __forceinline__ static unsigned short bits(float v) { return __half_as_ushort(__float2half_rn(v)); }
+  __device__ __forceinline__ static float from_bits(unsigned short b) { return __half2float(__ushort_as_half(b)); }
 };
 template <>
 struct Elem<__nv_bfloat16> {
@@ -133,6 +139,8 @@ struct Elem<__nv_bfloat16> {
     return make_uint4(w[0], w[1], w[2], w[3]);
   }
   __device__ __forceinline__ static __nv_bfloat16 from_f32(float v) { return __float2bfloat16_rn(v); }
+  __device__ __forceinline__ static unsigned short bits(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
+  __device__ __forceinline__ static float from_bits(unsigned short b) { return __uint_as_float((unsigned)b << 16); }
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -1064,10 +1072,14 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
   const int npix = TH * TW;
   const T* gyt = reinterpret_cast<const T*>(smem + g.o_gy);
   T* const omt = reinterpret_cast<T*>(smem + g.o_om);
-  float* const gomt = reinterpret_cast<float*>(smem + g.o_gom);
   int* const cnt = reinterpret_cast<int*>(smem + g.o_cnt);
   int* const fill = reinterpret_cast<int*>(smem + g.o_slot);  // per-bin fill pointers (P3)
-  uint2* const ent = reinterpret_cast<uint2*>(smem + g.o_ent);
+  // bin entries (a, source pixel): fp32 -> 8 B {a, src}; fp16/bf16 -> 4 B {a rounded to T |
+  // src << 16} (the pull's FHFMA rounds a to T anyway, fma_chunk), half the shared memory
+  constexpr bool ENT8 = sizeof(T) == 4;
+  using Ent = typename std::conditional<ENT8, uint2, uint32_t>::type;
+  using EntPair = typename std::conditional<ENT8, uint4, uint2>::type;
+  Ent* const ent = reinterpret_cast<Ent*>(smem + g.o_ent);
   int* const wsum = reinterpret_cast<int*>(smem + g.o_wsum);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + g.o_bar);
   if (threadIdx.x == 0) {
@@ -1081,7 +1093,6 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
   const int px = (tid / (L * GC)) % TW;
   const int py = tid / (L * GC * TW);
   const bool slot_ok = py < TH;
-  const int item = (py * TW + px) * GC + gl;  // (pixel, group) index inside the tile
   const unsigned gmask = (L >= 32 ? 0xffffffffu : ((1u << L) - 1u)) << (lane & ~(L - 1));
   const int rot = g.rot_shift < 0 ? 0 : (((tid & 31) / L) >> g.rot_shift) & (CPL - 1);
   int co[CPL];
@@ -1143,25 +1154,26 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
     const T* row = omt + (py * TW + px) * g.seg + gl * 3 * K;
     float m[K];
     unsigned outside = 0;
-    // Sample k of this (pixel, group): halo-local floor corner (yl, xl), fractions, whether
-    // it lies inside the halo, and the in-image corners.  P1 and P3 both call this, so the
-    // contributions P1 counts are exactly the ones P3 files.
+    // Sample k of the item at tile position (qy, qx) whose offset_mask row is `rw`: halo-
+    // local floor corner (yl, xl), fractions, whether it lies inside the halo, and the
+    // in-image corners.  P1 and P3 both call this, so the contributions P1 counts are
+    // exactly the ones P3 files.
     struct Pt {
       int yl, xl;
       float fy, fx, hy, hx;  // fractions and 1 - fractions (R11)
       bool fin, in, ok[4];
     };
-    auto point = [&](int k) {
+    auto point_at = [&](const T* rw, int qy, int qx, int k) {
       Pt P;
       const int i = k / 3, j = k % 3;
-      const float dx = Elem<T>::f(row[2 * k]), dy = Elem<T>::f(row[2 * k + 1]);
+      const float dx = Elem<T>::f(rw[2 * k]), dy = Elem<T>::f(rw[2 * k + 1]);
       bool finy, finx;
       int fly, flx;
       split_t<UNIT>(s, j - 1, dy, finy, fly, P.fy, P.hy);
       split_t<UNIT>(s, i - 1, dx, finx, flx, P.fx, P.hx);
       P.fin = finy && finx;
-      const int yl = py + (UNIT ? j + 2 : 3) + fly;
-      const int xl = px + (UNIT ? i + 2 : 3) + flx;
+      const int yl = qy + (UNIT ? j + 2 : 3) + fly;
+      const int xl = qx + (UNIT ? i + 2 : 3) + flx;
       P.in = P.fin && (unsigned)yl <= (unsigned)(HH - 2) && (unsigned)xl <= (unsigned)(HWC - 2);
       P.yl = P.in ? yl : 0;
       P.xl = P.in ? xl : 0;
@@ -1174,13 +1186,33 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       P.ok[3] = P.in && vy1 && vx1;
       return P;
     };
-    // ---- P1: bin counts only (coordinates, no data): shared-memory reductions
-    if (active) {
-      load_m<T, K>(row, g.softmax, m);
+    auto point = [&](int k) { return point_at(row, py, px, k); };
+    if (active) load_m<T, K>(row, g.softmax, m);
+    // ---- P1: bin counts only (coordinates, no data): shared-memory integer reductions.
+    // DCNv4: one thread per (item, sample) over the whole tile (the L lanes of an item do
+    // not repeat each other's coordinate work); DCNv3 softmax: each item's lanes (m needs
+    // the softmax over all K of the item).
+    if (!g.softmax && L >= 2) {
+      const int nsamp = npix * GC * K;
+      for (int sidx = tid; sidx < nsamp; sidx += blockDim.x) {
+        const int it9 = (sidx * 7282) >> 16;  // sidx / 9 (exact for sidx < 9216)
+        const int k = sidx - it9 * 9;
+        const int sgl = it9 % GC, spix = it9 / GC;
+        const int sy = spix / TW, sx = spix % TW;
+        if (h0 + sy >= g.Ho || w0 + sx >= g.Wo) continue;
+        const T* rw = omt + spix * g.seg + sgl * 3 * K;
+        const Pt P = point_at(rw, sy, sx, k);
+        const float mk = Elem<T>::f(rw[2 * K + k]);
+        const float w[4] = {P.hy * P.hx, P.hy * P.fx, P.fy * P.hx, P.fy * P.fx};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (P.ok[q] && mk * w[q] != 0.f)
+            atomicAdd(&cnt[sgl * NT + (P.yl + (q >> 1)) * HWC + P.xl + (q & 1)], 1);
+      }
+    } else if (active) {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const Pt P = point(k);
-        outside |= (P.fin && !P.in) ? (1u << k) : 0u;
         const float w[4] = {P.hy * P.hx, P.hy * P.fx, P.fy * P.hx, P.fy * P.fx};
 #pragma unroll
         for (int r = 0; r < QPL; ++r) {
@@ -1202,8 +1234,12 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
       for (int i = tid; i < GC * NT; i += blockDim.x) fill[i] = offs[i] & ~1;
       __syncthreads();
     }
-    // ---- P3: gathers from the x halo, grad_om partials, and filing of the contributions
+    // ---- P3: gathers from the x halo, grad_om (written straight to memory from the
+    // lanes), and filing of the contributions
     if (active) {
+      // this item's grad_offset_mask row: lane 0 writes d/d dx and d/d m, lane 1 d/d dy
+      T* const grow = gom + ((long long)(n * g.Ho + ho) * g.Wo + wo) * g.S + (g0 + gl) * 3 * K;
+      float gmv[K];
       float gyv[CPL * E];
       uint4 gyu[CPL];  // the lane's gy chunks, packed (dot products)
 #pragma unroll
@@ -1215,6 +1251,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const Pt P = point(k);
+        outside |= (P.fin && !P.in) ? (1u << k) : 0u;
         const uint32_t off = (uint32_t)(P.yl * ROWB + P.xl * PB);
         float S[4];
         float2 S2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -1240,11 +1277,14 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           sgy += __shfl_xor_sync(gmask, sgy, o);
           sgx += __shfl_xor_sync(gmask, sgx, o);
         }
-        if (lg == 0) {
-          float* grow = gomt + item * 3 * K;
-          grow[2 * k] = P.in ? s * m[k] * sgx : 0.f;
-          grow[2 * k + 1] = P.in ? s * m[k] * sgy : 0.f;
-          grow[2 * K + k] = P.in ? sgm : 0.f;
+        gmv[k] = P.in ? sgm : 0.f;
+        // d/d dx_k, d/d dy_k (samples beyond the halo are written by the global path below)
+        if (L >= 2) {
+          if (lg < 2 && !(P.fin && !P.in))
+            grow[2 * k + lg] = Elem<T>::from_f32(P.in ? s * m[k] * (lg ? sgy : sgx) : 0.f);
+        } else if (!(P.fin && !P.in)) {
+          grow[2 * k] = Elem<T>::from_f32(P.in ? s * m[k] * sgx : 0.f);
+          grow[2 * k + 1] = Elem<T>::from_f32(P.in ? s * m[k] * sgy : 0.f);
         }
         // file this lane's scatter contributions into their bins
 #pragma unroll
@@ -1254,7 +1294,8 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           if (lg < 4 && q < 4 && pick4(P.ok, q) && a != 0.f) {
             const int tt = (P.yl + (q >> 1)) * HWC + P.xl + (q & 1);
             const int e = atomicAdd(&fill[gl * NT + tt], 1);
-            ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
+            if constexpr (ENT8) ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
+            else ent[e] = (uint32_t)Elem<T>::bits(a) | ((uint32_t)(py * TW + px) << 16);
           }
         }
       }
@@ -1316,38 +1357,41 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
             sgy += __shfl_xor_sync(gmask, sgy, o);
             sgx += __shfl_xor_sync(gmask, sgx, o);
           }
-          if (lg == 0) {
-            float* grow = gomt + item * 3 * K;
-            grow[2 * k] = s * mk * sgx;
-            grow[2 * k + 1] = s * mk * sgy;
-            grow[2 * K + k] = sgm;
+          if (lg == 0) {  // the same thread reads these back below (program order)
+            grow[2 * k] = Elem<T>::from_f32(s * mk * sgx);
+            grow[2 * k + 1] = Elem<T>::from_f32(s * mk * sgy);
+            grow[2 * K + k] = Elem<T>::from_f32(sgm);
           }
         }
       }
-      if (g.softmax && lg == 0) {  // dL/dz_k = p_k (gm_k - sum_j p_j gm_j)
-        float* grow = gomt + item * 3 * K;
-        float dot = 0.f;
+      if (lg == 0) {  // d/d m_k (DCNv3: w.r.t. the logits, dL/dz_k = p_k (gm_k - sum_j p_j gm_j))
+        if (outside) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) dot += m[k] * grow[2 * K + k];
+          for (int k = 0; k < K; ++k)
+            if ((outside >> k) & 1u) gmv[k] = Elem<T>::f(grow[2 * K + k]);
+        }
+        if (g.softmax) {
+          float dot = 0.f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) grow[2 * K + k] = m[k] * (grow[2 * K + k] - dot);
+          for (int k = 0; k < K; ++k) dot += m[k] * gmv[k];
+#pragma unroll
+          for (int k = 0; k < K; ++k) gmv[k] = m[k] * (gmv[k] - dot);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) grow[2 * K + k] = Elem<T>::from_f32(gmv[k]);
+      }
+    }
+    // padding channels [3GK, S) of grad_offset_mask: written 0 by the last group run
+    if (g0 + GC == g.G && g.S > g.G * 3 * K) {
+      const int npad = g.S - g.G * 3 * K;
+      for (int f = tid; f < npix * npad; f += blockDim.x) {
+        const int p = f / npad, e = f - p * npad;
+        const int pho = h0 + p / TW, pwo = w0 + p % TW;
+        if (pho < g.Ho && pwo < g.Wo)
+          gom[((long long)(n * g.Ho + pho) * g.Wo + pwo) * g.S + g.G * 3 * K + e] = Elem<T>::from_f32(0.f);
       }
     }
     __syncthreads();
-    // ---- grad_om tile write-out (coalesced, warp per pixel); the last group run also
-    // zeroes the padding channels [3GK, S)
-    {
-      const bool last = g0 + GC == g.G;
-      for (int p = tid >> 5; p < npix; p += blockDim.x >> 5) {
-        const int pho = h0 + p / TW, pwo = w0 + p % TW;
-        if (pho >= g.Ho || pwo >= g.Wo) continue;
-        T* dst = gom + ((long long)(n * g.Ho + pho) * g.Wo + pwo) * g.S;
-        for (int e = lane; e < GC * 3 * K; e += 32)
-          dst[g0 * 3 * K + e] = Elem<T>::from_f32(gomt[p * GC * 3 * K + e]);
-        if (last)
-          for (int e = g.G * 3 * K + lane; e < g.S; e += 32) dst[e] = Elem<T>::from_f32(0.f);
-      }
-    }
     // ---- P4: pull per (halo pixel, group, PC chunks) and one vector reduction per chunk;
     // PC = 2 chunks per lane amortise the entry loads; the chunk order alternates with
     // the halo pixel so an 8-lane phase still touches 8 distinct bank quads
@@ -1366,7 +1410,19 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
         const int np = ((offs[gg * NT + tt + 1] & ~1) - b0) >> 1;  // entry pairs (last may be half)
         if (np == 0) continue;
         const bool odd = o0 & 1;
-        const uint4* b = reinterpret_cast<const uint4*>(ent + b0);
+        const EntPair* b = reinterpret_cast<const EntPair*>(ent + b0);
+        // decoded entry pair: weights and source pixels
+        struct Dec { float a0, a1; unsigned s0, s1; };
+        auto dec = [&](const EntPair& en) {
+          Dec d;
+          if constexpr (ENT8) {
+            d.a0 = __uint_as_float(en.x); d.s0 = en.y; d.a1 = __uint_as_float(en.z); d.s1 = en.w;
+          } else {
+            d.a0 = Elem<T>::from_bits((unsigned short)(en.x & 0xffffu)); d.s0 = en.x >> 16;
+            d.a1 = Elem<T>::from_bits((unsigned short)(en.y & 0xffffu)); d.s1 = en.y >> 16;
+          }
+          return d;
+        };
         int cc[PC];
 #pragma unroll
         for (int h = 0; h < PC; ++h) cc[h] = (cl * PC + ((h + rk) & (PC - 1))) * E;
@@ -1378,12 +1434,12 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
 #pragma unroll
           for (int e = 0; e < PC * E; ++e) acc[e] = 0;
           for (int q = 0; q < np; ++q) {
-            const uint4 en = b[q];
+            const Dec en = dec(b[q]);
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
               if (r == 1 && odd && q == np - 1) break;
-              const T* src = gyg + (r ? en.w : en.y) * (GC * DG);
-              const float ap = (__uint_as_float(r ? en.z : en.x) * ds.s1) * ds.s2;
+              const T* src = gyg + (r ? en.s1 : en.s0) * (GC * DG);
+              const float ap = ((r ? en.a1 : en.a0) * ds.s1) * ds.s2;
 #pragma unroll
               for (int h = 0; h < PC; ++h) {
                 float v[E];
@@ -1402,25 +1458,27 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           float acc[PC * E];
 #pragma unroll
           for (int e = 0; e < PC * E; ++e) acc[e] = 0.f;
-          // full pairs (branch-free, unrolled by the compiler), then the last pair
+          // full pairs (branch-free; unrolled so the entry and gy loads of several pairs
+          // are in flight together), then the last pair
+#pragma unroll 4
           for (int q = 0; q < np - 1; ++q) {
-            const uint4 en = b[q];
-            const T* src0 = gyg + en.y * (GC * DG);
-            const T* src1 = gyg + en.w * (GC * DG);
+            const Dec en = dec(b[q]);
+            const T* src0 = gyg + en.s0 * (GC * DG);
+            const T* src1 = gyg + en.s1 * (GC * DG);
 #pragma unroll
             for (int h = 0; h < PC; ++h) {
-              fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src0 + cc[h]));
-              fma_chunk<T>(acc + h * E, __uint_as_float(en.z), *reinterpret_cast<const uint4*>(src1 + cc[h]));
+              fma_chunk<T>(acc + h * E, en.a0, *reinterpret_cast<const uint4*>(src0 + cc[h]));
+              fma_chunk<T>(acc + h * E, en.a1, *reinterpret_cast<const uint4*>(src1 + cc[h]));
             }
           }
           {
-            const uint4 en = b[np - 1];
-            const T* src0 = gyg + en.y * (GC * DG);
-            const T* src1 = gyg + (odd ? 0u : en.w) * (GC * DG);
-            const float a1 = odd ? 0.f : __uint_as_float(en.z);
+            const Dec en = dec(b[np - 1]);
+            const T* src0 = gyg + en.s0 * (GC * DG);
+            const T* src1 = gyg + (odd ? 0u : en.s1) * (GC * DG);
+            const float a1 = odd ? 0.f : en.a1;
 #pragma unroll
             for (int h = 0; h < PC; ++h) {
-              fma_chunk<T>(acc + h * E, __uint_as_float(en.x), *reinterpret_cast<const uint4*>(src0 + cc[h]));
+              fma_chunk<T>(acc + h * E, en.a0, *reinterpret_cast<const uint4*>(src0 + cc[h]));
               fma_chunk<T>(acc + h * E, a1, *reinterpret_cast<const uint4*>(src1 + cc[h]));
             }
           }
