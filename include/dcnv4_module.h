@@ -76,6 +76,57 @@ DCNV4_API int dcnv4_module_forward(const dcnv4_params *p, dcnv4_dtype dtype, con
                                    const void *weight, const void *bias, void *output,
                                    void *stream);
 
+
+/* Module core forward with a separate value tensor (the full module, P:198 / P:1006-1009:
+ * a 1x1 input projection produces the value the operator samples, while the offset/mask
+ * linear reads the module input -- reading R22):
+ *   y = DCNv4(value, RN_T(input . weight^T + bias))
+ * Same kernel, requirements and arithmetic as dcnv4_module_forward (which is this call
+ * with value = input); value [N][H][W][G*D] T, 16-B aligned; output must not alias value
+ * (INVALID_ARG) or input.                                                               */
+DCNV4_API int dcnv4_module_core_forward(const dcnv4_params *p, dcnv4_dtype dtype, const void *input,
+                                        const void *value, const void *weight, const void *bias,
+                                        void *output, void *stream);
+
+/* ------------------------------------------------------------------------------------
+ * Dense layers of the full module and their backward (tcgen05 GEMMs, csrc/gemm.cu).
+ * All three take row-major T matrices (F16/BF16 only; F32 -> UNSUPPORTED), fp32
+ * accumulation in tensor memory, one persistent launch (+ the small launches noted);
+ * every pointer 16-B aligned (bias / grad_bias 2-B) else MISALIGNED; every channel count
+ * and leading dimension a multiple of 8 (16-B rows) else UNSUPPORTED; M < 2^31.
+ * Bit-deterministic except dcnv4_linear_grad_weight (fp32 reductions over K splits).    */
+
+/* y[M][N] = RN_T(x[M][K] . weight[N][K]^T + bias[N])  (nn.Linear layout; the module's
+ * 1x1 input / output projections).  bias may be NULL.               */
+DCNV4_API int dcnv4_linear(dcnv4_dtype dtype, int64_t M, int32_t K, int32_t N, const void *x,
+                           const void *weight, const void *bias, void *y, void *stream);
+
+/* grad_input of one or two linear layers that read the same input (the module's input
+ * feeds both the input projection and the offset/mask linear):
+ *   gx[M][K] = RN_T( gy0[M][0:N0] . weight0[N0][K]  +  gy1[M][N1] . weight1[N1][K] )
+ * gy0 has leading dimension ld0 >= N0 (e.g. grad_offset_mask [R][S], S >= 3GK, whose
+ * padding columns must be finite: they meet zero rows); N1 = 0 drops the second term
+ * (gy1, weight1 ignored).  The weights are read in their stored [N][K] layout (MN-major
+ * operands of the tensor-core MMA), no transposed copy.                                 */
+DCNV4_API int dcnv4_linear_grad_input(dcnv4_dtype dtype, int64_t M, int32_t K, int32_t N0,
+                                      const void *gy0, int32_t ld0, const void *weight0, int32_t N1,
+                                      const void *gy1, const void *weight1, void *gx, void *stream);
+
+/* Workspace (fp32 accumulators) dcnv4_linear_grad_weight needs: (N*K + N) * 4 bytes.     */
+DCNV4_API size_t dcnv4_linear_grad_weight_workspace_bytes(int32_t K, int32_t N);
+
+/* grad_weight and grad_bias of y = x . weight^T + bias over M rows:
+ *   grad_weight[N][K] = RN_T(sum_m gy[m][n] x[m][k]),  grad_bias[N] = RN_T(sum_m gy[m][n])
+ * gy [M][ld_gy] (first N columns used; N need not be a multiple of 8, e.g. N = 3GK of the
+ * offset/mask linear with gy = grad_offset_mask of row stride S), x [M][K].  The
+ * contraction over all M rows is
+ * split across CTAs and summed in fp32 (16-B vector reductions) into the workspace, then
+ * rounded once to T.  grad_bias may be NULL.  Launches: a workspace memset, the GEMM,
+ * a column-sum kernel (grad_bias) and the fp32 -> T conversion(s).                      */
+DCNV4_API int dcnv4_linear_grad_weight(dcnv4_dtype dtype, int64_t M, int32_t K, int32_t N, const void *x,
+                                       const void *gy, int32_t ld_gy, void *grad_weight, void *grad_bias,
+                                       void *workspace, size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

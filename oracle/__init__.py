@@ -313,3 +313,101 @@ def module_forward(geom: Geometry, x, weight, bias, dtype: str = "f32", with_abs
         return forward(geom, xf, om)
     y, ya = forward(geom, xf, om, with_abs=True)
     return y, ya, om
+
+
+# ---------------------------------------------------------------------------------------
+# The full DCNv4 module (R21, R22).  P:198: "A 1x1
+# point-wise convolution on x and y can be applied before and after" the spatial
+# aggregation; the offsets and aggregation weights come from one linear layer;
+# this full module (with the projections) is the one used in the rest of the
+# models.  Reading R22: the projected value v = x W_in^T + b_in is what the operator
+# samples, while the offset/mask linear reads the module input x (prior-art DCNv3/v4
+# module wiring; the paper does not draw the module).  Every layer's output is stored in
+# the storage dtype T between layers (R21 extended: what an unfused module holds in
+# memory), so each is rounded once, fp64 -> T.  dtype "f64" disables the rounding.
+
+def _rt(v, dtype):
+    return np.asarray(v, dtype=np.float64) if dtype == "f64" else round_to(v, dtype)
+
+
+def linear(x, weight, bias=None, dtype: str = "f64"):
+    """y = round_T(x @ weight^T + bias): nn.Linear / a 1x1 convolution in fp64.
+    x [R, K], weight [N, K], bias [N] or None."""
+    x, w = _f64(x), _f64(weight)
+    y = x @ w.T
+    if bias is not None:
+        y = y + _f64(bias).reshape(1, -1)
+    return _rt(y, dtype)
+
+
+def linear_abs(x_abs, weight, bias=None):
+    """Magnitude scale of linear(): |x| @ |W|^T + |b| (SURVEY 8(c).4 metric, chained)."""
+    y = _f64(x_abs) @ np.abs(_f64(weight)).T
+    if bias is not None:
+        y = y + np.abs(_f64(bias)).reshape(1, -1)
+    return y
+
+
+def module_full_forward(geom: Geometry, x, params: dict, dtype: str = "f64", with_abs: bool = False):
+    """Full DCNv4 module forward: v = linear(x; W_in, b_in), om = linear(x; W_om, b_om)
+    (padded to S channels with zeros), a = DCNv4(v, om) (Eq. (1)-(2)),
+    y = linear(a; W_out, b_out); each output rounded to T (R22).  params: w_in, b_in,
+    w_om, b_om, w_out, b_out (biases may be None).  Stride-1 'same' geometry.
+    Returns a dict with v, om, a, y (fp64 arrays in NHWC) and, with_abs, y_abs / a_abs."""
+    Ho, Wo = geom.out_hw()
+    if (Ho, Wo) != (geom.H, geom.W):
+        raise ValueError("the full module needs Ho == H and Wo == W")
+    R = geom.N * geom.H * geom.W
+    xf = _f64(x).reshape(R, geom.C)
+    v = linear(xf, params["w_in"], params.get("b_in"), dtype)
+    J = _f64(params["w_om"]).shape[0]
+    om = np.zeros((R, geom.S))
+    om[:, :J] = linear(xf, params["w_om"], params.get("b_om"), dtype)
+    om = om.reshape(geom.N, Ho, Wo, geom.S)
+    out = {"v": v.reshape(geom.N, geom.H, geom.W, geom.C), "om": om}
+    if with_abs:
+        a, a_abs0 = forward(geom, v, om, with_abs=True)
+        v_abs = linear_abs(np.abs(xf), params["w_in"], params.get("b_in"))
+        # DCNv4 magnitude pass over the value magnitudes: sum |m| w v_abs
+        _, a_abs = forward(geom, v_abs, om, with_abs=True)
+        a = _rt(a, dtype)
+        out["a_abs"] = a_abs
+        out["y_abs"] = linear_abs(a_abs.reshape(R, geom.C), params["w_out"], params.get("b_out")).reshape(
+            geom.N, Ho, Wo, -1)
+    else:
+        a = _rt(forward(geom, v, om), dtype)
+    out["a"] = a
+    out["y"] = linear(a.reshape(R, geom.C), params["w_out"], params.get("b_out"), dtype).reshape(
+        geom.N, Ho, Wo, -1)
+    return out
+
+
+def module_full_backward(geom: Geometry, x, params: dict, gy, dtype: str = "f64"):
+    """Backward of module_full_forward given gy = dL/dy, each stored result rounded to T
+    (R22): ga = gy @ W_out, (gv, gom) = DCNv4 backward, and for each
+    linear y = x W^T + b: dx = dy @ W, dW = dy^T @ x, db = sum_rows dy.  The module input
+    feeds both the input projection and the offset/mask linear, so
+    gx = gv @ W_in + gom[:, :J] @ W_om.  Returns a dict of fp64 arrays."""
+    fw = module_full_forward(geom, x, params, dtype)
+    R = geom.N * geom.H * geom.W
+    xf = _f64(x).reshape(R, geom.C)
+    gyf = _f64(gy).reshape(R, -1)
+    a = fw["a"].reshape(R, geom.C)
+    w_out, w_in, w_om = _f64(params["w_out"]), _f64(params["w_in"]), _f64(params["w_om"])
+    J = w_om.shape[0]
+    g = {}
+    g["w_out"] = _rt(gyf.T @ a, dtype)
+    g["b_out"] = _rt(gyf.sum(axis=0), dtype)
+    ga = _rt(gyf @ w_out, dtype)
+    gv, gom = backward(geom, fw["v"], fw["om"], ga.reshape(geom.N, geom.H, geom.W, geom.C))
+    gv = _rt(gv.reshape(R, geom.C), dtype)
+    gom = _rt(gom.reshape(R, geom.S), dtype)
+    g["w_in"] = _rt(gv.T @ xf, dtype)
+    g["b_in"] = _rt(gv.sum(axis=0), dtype)
+    g["w_om"] = _rt(gom[:, :J].T @ xf, dtype)
+    g["b_om"] = _rt(gom[:, :J].sum(axis=0), dtype)
+    g["x"] = _rt(gv @ w_in + gom[:, :J] @ w_om, dtype).reshape(geom.N, geom.H, geom.W, geom.C)
+    g["a"] = ga.reshape(geom.N, geom.H, geom.W, geom.C)
+    g["v"] = gv.reshape(geom.N, geom.H, geom.W, geom.C)
+    g["om"] = gom.reshape(geom.N, geom.H, geom.W, geom.S)
+    return g

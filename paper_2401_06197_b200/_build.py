@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libdcnv4.so")
-SOURCES = ["dcnv4_api.cu", "dcnv4_f32.cu", "dcnv4_f16.cu", "dcnv4_bf16.cu", "msda.cu", "om_linear.cu", "module_fwd.cu"]
+SOURCES = ["dcnv4_api.cu", "dcnv4_f32.cu", "dcnv4_f16.cu", "dcnv4_bf16.cu", "msda.cu", "om_linear.cu", "module_fwd.cu", "gemm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

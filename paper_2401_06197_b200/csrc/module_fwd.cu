@@ -389,10 +389,11 @@ cudaError_t launch_module_t(int nch, const CUtensorMap& hm, const CUtensorMap& a
 
 }  // namespace oml
 
-extern "C" {
-
-int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input, const void* weight,
-                         const void* bias, void* output, void* stream) {
+namespace oml {
+// y = DCNv4(value, RN_T(input . W^T + b)): the offset_mask from `input`, the samples from
+// `value` (the lightweight module: value == input)
+static int module_forward_impl(const dcnv4_params* p, dcnv4_dtype dtype, const void* input, const void* value,
+                               const void* weight, const void* bias, void* output, void* stream) {
   using namespace oml;
   int64_t Ho = 0, Wo = 0;
   int rc = dcnv4_output_size(p, &Ho, &Wo);
@@ -417,9 +418,9 @@ int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* i
     return fail(DCNV4_ERR_SHAPE, "input too large");
   if (p->H * p->W * C >= (1LL << 31)) return fail(DCNV4_ERR_SHAPE, "per-image size H*W*C must be < 2^31");
   if (p->N == 0) return DCNV4_OK;
-  if (!input || !weight || !output)
-    return fail(DCNV4_ERR_INVALID_ARG, "%s is NULL", !input ? "input" : !weight ? "weight" : "output");
-  if (((uintptr_t)input | (uintptr_t)weight | (uintptr_t)output) & 15)
+  if (!input || !value || !weight || !output)
+    return fail(DCNV4_ERR_INVALID_ARG, "%s is NULL", !input ? "input" : !value ? "value" : !weight ? "weight" : "output");
+  if (((uintptr_t)input | (uintptr_t)value | (uintptr_t)weight | (uintptr_t)output) & 15)
     return fail(DCNV4_ERR_MISALIGNED, "%s is not 16-B aligned",
                 ((uintptr_t)input & 15) ? "input" : ((uintptr_t)weight & 15) ? "weight" : "output");
   if ((uintptr_t)bias & 1) return fail(DCNV4_ERR_MISALIGNED, "bias is not 2-B aligned");
@@ -480,7 +481,7 @@ int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* i
                       8 * (2 * g.stages + 2) + 16;
   if (smem > 227 * 1024) return fail(DCNV4_ERR_UNSUPPORTED, "shared-memory plan exceeds 227 KB");
   CUtensorMap hm, am, bm;
-  CUresult e1 = encode4d(&hm, dtype, input, p->N, p->H, p->W, C, GC * p->D, 14, 22, false);
+  CUresult e1 = encode4d(&hm, dtype, value, p->N, p->H, p->W, C, GC * p->D, 14, 22, false);
   CUresult e2 = encode4d(&am, dtype, input, p->N, p->H, p->W, C, BK, 8, 16, true);
   CUresult e3 = encode2d(&bm, dtype, weight, J, C, BK, g.BN);
   if (e1 != CUDA_SUCCESS || e2 != CUDA_SUCCESS || e3 != CUDA_SUCCESS)
@@ -488,10 +489,27 @@ int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* i
   const bool unit = p->offset_scale == 1.0f;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t err = dtype == DCNV4_F16
-                        ? launch_module_t<__half>(nch, hm, am, bm, g, unit, smem, input, bias, output, st)
-                        : launch_module_t<__nv_bfloat16>(nch, hm, am, bm, g, unit, smem, input, bias, output, st);
+                        ? launch_module_t<__half>(nch, hm, am, bm, g, unit, smem, value, bias, output, st)
+                        : launch_module_t<__nv_bfloat16>(nch, hm, am, bm, g, unit, smem, value, bias, output, st);
   if (err != cudaSuccess) return fail(DCNV4_ERR_CUDA, "module_fwd launch: %s", cudaGetErrorString(err));
   return DCNV4_OK;
+}
+}  // namespace oml
+
+extern "C" {
+
+int dcnv4_module_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input, const void* weight,
+                         const void* bias, void* output, void* stream) {
+  return oml::module_forward_impl(p, dtype, input, input, weight, bias, output, stream);
+}
+
+int dcnv4_module_core_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input, const void* value,
+                              const void* weight, const void* bias, void* output, void* stream) {
+  if (value == output && value) {
+    dcnv4_internal_set_error("dcnv4_module_core_forward: output must not alias value");
+    return DCNV4_ERR_INVALID_ARG;
+  }
+  return oml::module_forward_impl(p, dtype, input, value, weight, bias, output, stream);
 }
 
 }  // extern "C"
