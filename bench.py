@@ -92,6 +92,16 @@ WORKLOADS = {
     "module_c3": dict(desc="NEXT-2 fused lightweight module forward on the 800x1280 stage "
                            "shapes, D=16, fp16, batch 8", stages=STAGES_800, dtype="f16", batch=8,
                       backward=False, shard=False, module=True),
+    # NEXT-2, full module (R22): input projection, fused om-linear + aggregation sampling
+    # the projection, output projection; backward = every GEMM's grads + DCNv4 backward
+    "module_full_c2": dict(desc="NEXT-2 full DCNv4 module (1x1 in/out projections, P:198, "
+                                "P:1006-1009) forward, 224^2 stage shapes, D=16, fp16, batch 64",
+                           stages=STAGES_224, dtype="f16", batch=64, backward=False, shard=False,
+                           module="full"),
+    "module_full_train_c2": dict(desc="NEXT-2 full DCNv4 module forward + backward (all weight and "
+                                      "input gradients), 224^2 stage shapes, D=16, fp16, batch 64",
+                                 stages=STAGES_224, dtype="f16", batch=64, backward=True, shard=False,
+                                 module="full"),
 }
 # forward sweeps measured by the default run (workload, batch override)
 EXTRAS = [("c2_f32", None), ("c2_f16", None), ("c3_f16", 1), ("c3_f16", 8), ("c2p_f32", None),
@@ -247,6 +257,22 @@ def _alg_bytes(x, om, backward, w=None):
     return (3 * bx + 2 * bo) if backward else (2 * bx + bo)
 
 
+def _call_bytes(cfg, st, kind):
+    """Algorithmic bytes of one call of a stage: _alg_bytes for the operator / lightweight
+    module; for the full module (R22) every tensor each GEMM / kernel must read or write
+    once (A = activation bytes [N,H,W,C], O = offset_mask bytes [N,H,W,S], Wt = weights):
+      fwd          v = lin(x), a = core(x, v), y = lin(a):      7A + Wt
+      fwd_unfused  + om = lin(x) written and read back:         6A + 2O + Wt
+      bwd          ga, dW_out, om recompute, DCNv4 bwd, gx, dW_in, dW_om:  13A + 5O + 2 Wt"""
+    if cfg.get("module") != "full":
+        return _alg_bytes(st["x"], st["om"], kind == "bwd", st.get("w"))
+    A = st["x"].numel() * st["x"].element_size()
+    S = -(-27 * st["G"] // 8) * 8
+    O = A // st["x"].shape[-1] * S
+    Wt = sum(v.numel() * v.element_size() for v in st["params"].values())
+    return {"fwd": 7 * A + Wt, "fwd_unfused": 6 * A + 2 * O + Wt, "bwd": 13 * A + 5 * O + 2 * Wt}[kind]
+
+
 def _traffic(workload, kind):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -268,6 +294,10 @@ def oracle_inputs(cfg, images):
         g = oracle.Geometry(N=len(images), H=H, W=W, G=G, D=D)
         x, om, gy = synth.make_case(len(images), H, W, G, D, H, W, K, 27 * G, cfg["dtype"],
                                     images=images)
+        if cfg.get("module") == "full":
+            prm = {k: oracle._f64(v) for k, v in synth.make_module_params(G * D, G, K, cfg["dtype"]).items()}
+            data.append((g, oracle._f64(x), prm, oracle._f64(gy)))
+            continue
         if cfg.get("module"):  # om comes from the linear: carry (weight, bias) instead
             w, b = synth.make_linear(G * D, G, K, cfg["dtype"])
             om = (oracle._f64(w), oracle._f64(b))
@@ -283,6 +313,12 @@ def oracle_sample(cfg, data):
     import oracle
     t0 = time.perf_counter()
     for g, x, om, gy in data:
+        if cfg.get("module") == "full":
+            if cfg["backward"]:
+                oracle.module_full_backward(g, x, om, gy, cfg["dtype"])  # includes the forward
+            else:
+                oracle.module_full_forward(g, x, om, cfg["dtype"])
+            continue
         if cfg.get("module"):
             oracle.module_forward(g, x, om[0], om[1], cfg["dtype"])
             continue
@@ -361,11 +397,14 @@ def _make_stages(cfg, ctx, images, offsets, deterministic):
                                     images=images, offsets=offsets, with_gy=cfg["backward"])
         st = dict(H=H, W=W, G=G, D=D, x_cpu=x, om_cpu=om, gy_cpu=gy, x=x.to(dev), om=om.to(dev),
                   gy=gy.to(dev) if gy is not None else None)
-        if cfg.get("module"):
+        if cfg.get("module") == "full":
+            prm = synth.make_module_params(G * D, G, K, cfg["dtype"])
+            st.update(params_cpu=prm, params={k: v.to(dev) for k, v in prm.items()})
+        elif cfg.get("module"):
             w, b = synth.make_linear(G * D, G, K, cfg["dtype"])
             st.update(w_cpu=w, b_cpu=b, w=w.to(dev), b=b.to(dev))
         st["y"] = torch.empty_like(st["x"])
-        if cfg["backward"]:
+        if cfg["backward"] and cfg.get("module") != "full":
             st["gx"] = torch.empty_like(st["x"])
             st["gom"] = torch.empty_like(st["om"])
             need = pkg.workspace_bytes(pkg.make_params(len(images), H, W, G, D,
@@ -376,6 +415,24 @@ def _make_stages(cfg, ctx, images, offsets, deterministic):
 
 
 def _calls(cfg, st, pkg, softmax, deterministic):
+    if cfg.get("module") == "full":
+        M = pkg.module
+
+        def fwd():
+            st["y"], st["saved"] = M.full_forward(st["x"], st["params"], st["G"], softmax=softmax)
+
+        def fwd_unfused():  # the multi-call path: 4 launches, om through memory
+            p = st["params"]
+            v = M.linear(st["x"], p["w_in"], p["b_in"])
+            om = M.offset_mask_linear(st["x"], p["w_om"], p["b_om"], st["G"])
+            a = pkg.forward(v, om, group=st["G"], softmax=softmax)
+            st["y_unfused"] = M.linear(a, p["w_out"], p["b_out"])
+
+        out = [("fwd", fwd), ("fwd_unfused", fwd_unfused)]
+        if cfg["backward"]:
+            out.append(("bwd", lambda: st.__setitem__("grads", M.full_backward(
+                st["x"], st["params"], st["G"], st["gy"], st["saved"], softmax=softmax))))
+        return out
     if cfg.get("module"):
         return [("fwd", lambda: pkg.module.forward_fused(st["x"], st["w"], st["b"], st["G"],
                                                          softmax=softmax, out=st["y"]))]
@@ -397,7 +454,8 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
     stages = _make_stages(cfg, ctx, images, offsets, deterministic)
     step_calls = [(si, kind, fn) for si, st in enumerate(stages)
                   for kind, fn in _calls(cfg, st, pkg, softmax, deterministic)]
-    work_set = sum(_alg_bytes(s["x"], s["om"], cfg["backward"], s.get("w")) for s in stages)
+    work_set = sum(_call_bytes(cfg, s, "fwd") + (_call_bytes(cfg, s, "bwd") if cfg["backward"] else 0)
+                   for s in stages)
     flush_bytes = 0
     if work_set < 2 * ctx.l2_bytes:
         # the step's data could stay in L2 between steps: write a 2xL2 buffer after every
@@ -478,9 +536,10 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
     flush_ms = 0.0
     for i, d in enumerate(durs):
         si, kind, _ = step_calls[i % n_calls]
-        if kind == "flush":
+        if kind in ("flush", "fwd_unfused"):  # timed separately, not part of the step
             flush_ms += d
-            continue
+            if kind == "flush":
+                continue
         per_call.setdefault((si, kind), []).append(d)
     flush_per_step = flush_ms / gsteps
     ms_step = max_over_ranks((total_ms - flush_per_step * steps) / steps, ws, ctx.dist, dev)
@@ -491,11 +550,11 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
     paper = PAPER_A100_MS.get(cfg.get("paper"), {}).get(cfg["dtype"])
     for si, st in enumerate(stages):
         row = {"shape": shape_name(st["H"], st["W"], st["G"], st["D"]), "images": len(images)}
-        for kind in ("fwd", "bwd"):
+        for kind in ("fwd", "bwd", "fwd_unfused"):
             if (si, kind) not in per_call:
                 continue
             ms = sum(per_call[(si, kind)]) / len(per_call[(si, kind)])
-            b = _alg_bytes(st["x"], st["om"], kind == "bwd", st.get("w"))
+            b = _call_bytes(cfg, st, kind)
             gbs = b / (ms * 1e-3) / 1e9
             srt = sorted(per_call[(si, kind)])
             pick = lambda q: srt[min(len(srt) - 1, int(q * (len(srt) - 1) + 0.5))]  # noqa: E731
@@ -503,13 +562,18 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
             row[f"{kind}_us_p10_p50_p90"] = [round(pick(q) * 1e3, 2) for q in (0.1, 0.5, 0.9)]
             row[f"{kind}_GBs"] = round(gbs, 1)
             row[f"{kind}_frac"] = round(gbs / peak, 4)
+            if kind == "fwd_unfused":  # reported beside the fused path, not part of the step
+                continue
             kind_bytes[kind] = kind_bytes.get(kind, 0) + b
             kind_ms[kind] = kind_ms.get(kind, 0.0) + ms
         if paper and si < len(paper):
             row["paper_a100_fwd_us"] = round(paper[si] * 1e3, 1)
         # checksum: fp64 sums of the outputs of the last step
         row["checksum"] = {"y": float(st["y"].double().sum())}
-        if cfg["backward"]:
+        if cfg.get("module") == "full":
+            if cfg["backward"]:
+                row["checksum"].update({f"grad_{k}": float(v.double().sum()) for k, v in st["grads"].items()})
+        elif cfg["backward"]:
             row["checksum"]["grad_offset_mask"] = float(st["gom"].double().sum())
             row["checksum"]["grad_input"] = float(st["gx"].double().sum())
         table.append(row)
@@ -517,8 +581,12 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
     launches_dom = len(stages)
     achieved = kind_bytes[dom] / (kind_ms[dom] * 1e-3) / 1e9
     share = kind_ms[dom] / sum(kind_ms.values())
-    kname = "memset + bwd33_kernel" if dom == "bwd" else (
-        "module_fwd_kernel: tcgen05 linear + aggregation" if cfg.get("module") else "fwd33_kernel")
+    if cfg.get("module") == "full":
+        kname = ("full-module backward: tcgen05 GEMMs + offset/mask linear + memset + bwd33_kernel"
+                 if dom == "bwd" else "full-module forward: tcgen05 linear + module_fwd_kernel + tcgen05 linear")
+    else:
+        kname = "memset + bwd33_kernel" if dom == "bwd" else (
+            "module_fwd_kernel: tcgen05 linear + aggregation" if cfg.get("module") else "fwd33_kernel")
     roofline = {"bound": "hbm", "kernel": f"dcnv4 {dom} ({kname}), {launches_dom} launches per step",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
@@ -541,13 +609,18 @@ def _verify(cfg, stages, images, softmax=False):
     tol = 1e-5 if cfg["dtype"] == "f32" else 1e-2
     for st in stages:
         g = oracle.Geometry(N=1, H=st["H"], W=st["W"], G=st["G"], D=st["D"], softmax=softmax)
+        if cfg.get("module") == "full":  # forward of the first image (weight grads sum the batch)
+            fw = oracle.module_full_forward(g, st["x_cpu"][:1], st["params_cpu"], cfg["dtype"], with_abs=True)
+            out[shape_name(st["H"], st["W"], st["G"], st["D"])] = {
+                "y": float(f"{oracle.abs_scaled_error(st['y'][:1].cpu(), fw['y'], fw['y_abs']):.3e}")}
+            continue
         if cfg.get("module"):
             y_ref, y_abs, _ = oracle.module_forward(g, st["x_cpu"][:1], st["w_cpu"], st["b_cpu"],
                                                     cfg["dtype"], with_abs=True)
         else:
             y_ref, y_abs = oracle.forward(g, st["x_cpu"][:1], st["om_cpu"][:1], with_abs=True)
         errs = {"y": oracle.abs_scaled_error(st["y"][:1].cpu(), y_ref, y_abs)}
-        if cfg["backward"]:
+        if cfg["backward"] and not cfg.get("module"):
             gx_ref, gom_ref, gxa, goma = oracle.backward(g, st["x_cpu"][:1], st["om_cpu"][:1],
                                                          st["gy_cpu"][:1], with_abs=True)
             errs["grad_input"] = oracle.abs_scaled_error(st["gx"][:1].cpu(), gx_ref, gxa)
@@ -593,9 +666,14 @@ def _e2e(args, cfg, stages, ctx):
         if cfg["backward"]:
             h["gy"] = st["gy_cpu"].pin_memory()
             h["gx"] = torch.empty_like(st["x_cpu"]).pin_memory()
-            h["gom"] = torch.empty_like(st["om_cpu"]).pin_memory()
             h2d += h["gy"].numel() * h["gy"].element_size()
-            d2h += sum(h[k].numel() * h[k].element_size() for k in ("gx", "gom"))
+            if cfg.get("module") == "full":  # grad_input and every weight / bias gradient
+                h["gw"] = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in st["params"].items()}
+                d2h += h["gx"].numel() * h["gx"].element_size() + sum(
+                    v.numel() * v.element_size() for v in h["gw"].values())
+            else:
+                h["gom"] = torch.empty_like(st["om_cpu"]).pin_memory()
+                d2h += sum(h[k].numel() * h[k].element_size() for k in ("gx", "gom"))
         host.append(h)
 
     # chunked over images on three streams (paper_2401_06197_b200/pipeline.py): the H2D
@@ -604,6 +682,8 @@ def _e2e(args, cfg, stages, ctx):
     from paper_2401_06197_b200.pipeline import HostPipeline
     nimg = len(stages[0]["x"])
     nch = max(1, min(args.e2e_chunks, nimg))
+    if cfg.get("module") == "full" and cfg["backward"]:
+        nch = 1  # the weight gradients sum over the whole batch: one chunk
     bounds = [(c * nimg // nch, (c + 1) * nimg // nch) for c in range(nch)]
     pipe = HostPipeline(dev, nch)
 
@@ -619,6 +699,14 @@ def _e2e(args, cfg, stages, ctx):
     def compute(c):
         lo, hi = bounds[c]
         for st in stages:
+            if cfg.get("module") == "full":
+                M = pkg.module
+                y, saved = M.full_forward(st["x"][lo:hi], st["params"], st["G"], softmax=args.softmax)
+                st["y"][lo:hi].copy_(y)
+                if cfg["backward"]:
+                    st["grads"] = M.full_backward(st["x"][lo:hi], st["params"], st["G"], st["gy"][lo:hi],
+                                                  saved, softmax=args.softmax)
+                continue
             if cfg.get("module"):
                 pkg.module.forward_fused(st["x"][lo:hi], st["w"], st["b"], st["G"],
                                          softmax=args.softmax, out=st["y"][lo:hi])
@@ -635,7 +723,11 @@ def _e2e(args, cfg, stages, ctx):
         lo, hi = bounds[c]
         for st, h in zip(stages, host):
             h["y"][lo:hi].copy_(st["y"][lo:hi], non_blocking=True)
-            if cfg["backward"]:
+            if cfg["backward"] and cfg.get("module") == "full":
+                h["gx"][lo:hi].copy_(st["grads"]["x"], non_blocking=True)
+                for k, v in h["gw"].items():
+                    v.copy_(st["grads"][k], non_blocking=True)
+            elif cfg["backward"]:
                 h["gx"][lo:hi].copy_(st["gx"][lo:hi], non_blocking=True)
                 h["gom"][lo:hi].copy_(st["gom"][lo:hi], non_blocking=True)
 
@@ -757,6 +849,25 @@ def main(argv=None):
         n_ours += 2 * len(stages)  # per-image maxima + int64 -> T conversion
     elif cfg["backward"] and cfg["dtype"] != "f32":
         n_ours += len(stages)  # fp32 -> half grad_input conversion
+    detail = (f"per step: {len(stages)} "
+              + ("module_fwd_kernel" if cfg.get("module") else "fwd33_kernel")
+              + (f" + {len(stages)} bwd33_kernel + {len(stages)} accumulator "
+                 f"zero-fill (cudaMemsetAsync)" if cfg["backward"] else "")
+              + (f" + {len(stages)} det_scale_kernel + {len(stages)} det_convert_kernel"
+                 if cfg["backward"] and args.deterministic else
+                 f" + {len(stages)} convert_kernel" if cfg["backward"] and cfg["dtype"] != "f32"
+                 else ""))
+    if cfg.get("module") == "full":
+        # per stage: forward 3 (gemm, module_fwd, gemm) + the unfused comparison path 4
+        # (gemm, om_linear, fwd33, gemm; its time is excluded from the step); backward 17
+        # (3 x grad_weight: gemm + colsum + 2 conversions; 2 grad_input gemms; om_linear;
+        # bwd33 + convert)
+        n_ours = len(stages) * (3 + 4 + (17 if cfg["backward"] else 0))
+        detail = (f"per stage and step: forward gemm_kernel + module_fwd_kernel + gemm_kernel; unfused "
+                  f"comparison gemm_kernel + om_linear_kernel + fwd33_kernel + gemm_kernel"
+                  + ("; backward 3 x (gemm_kernel + colsum_kernel + 2 f32_to_t_kernel) + 2 gemm_kernel + "
+                     "om_linear_kernel + bwd33_kernel + convert_kernel (+ 4 cudaMemsetAsync)"
+                     if cfg["backward"] else ""))
     Ds = sorted({d for *_, d in cfg["stages"]})
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "imgs/s", "n_gpus": ws,
@@ -776,14 +887,7 @@ def main(argv=None):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": n_ours * r["steps"],
-        "gpu_launch_detail": f"per step: {len(stages)} "
-                             + ("module_fwd_kernel" if cfg.get("module") else "fwd33_kernel")
-                             + (f" + {len(stages)} bwd33_kernel + {len(stages)} accumulator "
-                                f"zero-fill (cudaMemsetAsync)" if cfg["backward"] else "")
-                             + (f" + {len(stages)} det_scale_kernel + {len(stages)} det_convert_kernel"
-                                if cfg["backward"] and args.deterministic else
-                                f" + {len(stages)} convert_kernel" if cfg["backward"] and cfg["dtype"] != "f32"
-                                else ""),
+        "gpu_launch_detail": detail,
         "clocks": r["clocks"],
         "stages": r["table"],
         "parity": r["parity"],

@@ -137,3 +137,26 @@ def make_linear(C, G, K, dtype="f32", seed=0):
     g = torch.Generator().manual_seed(seed_of(TENSOR_BIAS, seed))
     b = torch.rand((J,), generator=g, dtype=torch.float32) - 0.5
     return w.to(DTYPES[dtype]), b.to(DTYPES[dtype])
+
+
+# Full-module projections (NEXT-2, R22): the 1x1 input / output projections of
+# P:198 drawn like an initialised layer, weight [C_out, C_in] ~ U(-1, 1) * sqrt(3 / C_in)
+# (unit-variance outputs for unit-variance inputs), bias ~ U(-0.1, 0.1).
+TENSOR_PROJ_W, TENSOR_PROJ_B = 22, 23
+
+
+def make_projection(C_out, C_in, dtype="f32", seed=0):
+    """CPU tensors (weight [C_out, C_in], bias [C_out]) in ``dtype``."""
+    g = torch.Generator().manual_seed(seed_of(TENSOR_PROJ_W, seed))
+    w = (torch.rand((C_out, C_in), generator=g, dtype=torch.float32) * 2.0 - 1.0) * (3.0 / C_in) ** 0.5
+    g = torch.Generator().manual_seed(seed_of(TENSOR_PROJ_B, seed))
+    b = (torch.rand((C_out,), generator=g, dtype=torch.float32) * 2.0 - 1.0) * 0.1
+    return w.to(DTYPES[dtype]), b.to(DTYPES[dtype])
+
+
+def make_module_params(C, G, K=9, dtype="f32", seed=0):
+    """The full module's parameters {w_in, b_in, w_om, b_om, w_out, b_out} (CPU)."""
+    w_in, b_in = make_projection(C, C, dtype, 2 * seed)
+    w_out, b_out = make_projection(C, C, dtype, 2 * seed + 1)
+    w_om, b_om = make_linear(C, G, K, dtype, seed)
+    return {"w_in": w_in, "b_in": b_in, "w_om": w_om, "b_om": b_om, "w_out": w_out, "b_out": b_out}
