@@ -84,6 +84,13 @@ WORKLOADS = {
     "c3p_f16": dict(desc="c3' (SURVEY 8(d).1): Tab. op_high_res shapes, D=32, fp16 forward, batch 1",
                     stages=STAGES_HIGH_D32, dtype="f16", batch=1, backward=False, shard=False,
                     paper="high"),
+    # all stages of one step in ONE persistent launch (dcnv4_forward_grouped)
+    "c3_f16_grouped": dict(desc="BASELINE configs[2] stages, D=16, fp16 forward, batch 8, the four "
+                                "stages in one dcnv4_forward_grouped launch", stages=STAGES_800,
+                           dtype="f16", batch=8, backward=False, shard=False, grouped=True),
+    "c2_f16_grouped": dict(desc="BASELINE configs[1] stages, D=16, fp16 forward, batch 64, the four "
+                                "stages in one dcnv4_forward_grouped launch", stages=STAGES_224,
+                           dtype="f16", batch=64, backward=False, shard=False, grouped=True),
     # NEXT-2 (R21): the lightweight DCNv4 module forward, one fused kernel per
     # stage (offset/mask linear on tcgen05 + aggregation; om never leaves the SM)
     "module_c2": dict(desc="NEXT-2 fused lightweight module forward (P:334, P:1003-1009) on the "
@@ -104,7 +111,8 @@ WORKLOADS = {
                                  module="full"),
 }
 # forward sweeps measured by the default run (workload, batch override)
-EXTRAS = [("c2_f32", None), ("c2_f16", None), ("c3_f16", 1), ("c3_f16", 8), ("c2p_f32", None),
+EXTRAS = [("c2_f32", None), ("c2_f16", None), ("c2_f16_grouped", None), ("c3_f16", 1),
+          ("c3_f16_grouped", 1), ("c3_f16", 8), ("c3_f16_grouped", 8), ("c2p_f32", None),
           ("c2p_f16", None), ("c3p_f32", None), ("c3p_f16", None), ("c5_bf16", None)]
 K = 9
 MIN_TIMED_S = 0.4      # auto step count: timed region >= this (>= 2 clock samples at 50 ms)
@@ -452,8 +460,14 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
     clocks sampled during the timed region and the parity record."""
     torch, pkg, dev, stream, ws, rank = ctx.torch, ctx.pkg, ctx.dev, ctx.stream, ctx.ws, ctx.rank
     stages = _make_stages(cfg, ctx, images, offsets, deterministic)
-    step_calls = [(si, kind, fn) for si, st in enumerate(stages)
-                  for kind, fn in _calls(cfg, st, pkg, softmax, deterministic)]
+    if cfg.get("grouped"):  # every stage in one dcnv4_forward_grouped launch
+        def grouped():
+            pkg.forward_grouped([s["x"] for s in stages], [s["om"] for s in stages], [s["G"] for s in stages],
+                                softmax=softmax, outs=[s["y"] for s in stages])
+        step_calls = [(0, "fwd", grouped)]
+    else:
+        step_calls = [(si, kind, fn) for si, st in enumerate(stages)
+                      for kind, fn in _calls(cfg, st, pkg, softmax, deterministic)]
     work_set = sum(_call_bytes(cfg, s, "fwd") + (_call_bytes(cfg, s, "bwd") if cfg["backward"] else 0)
                    for s in stages)
     flush_bytes = 0
@@ -550,11 +564,15 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
     paper = PAPER_A100_MS.get(cfg.get("paper"), {}).get(cfg["dtype"])
     for si, st in enumerate(stages):
         row = {"shape": shape_name(st["H"], st["W"], st["G"], st["D"]), "images": len(images)}
+        if cfg.get("grouped") and si == 0:
+            row["shape"] = "all stages, one grouped launch: " + ", ".join(
+                shape_name(q["H"], q["W"], q["G"], q["D"]) for q in stages)
         for kind in ("fwd", "bwd", "fwd_unfused"):
             if (si, kind) not in per_call:
                 continue
             ms = sum(per_call[(si, kind)]) / len(per_call[(si, kind)])
-            b = _call_bytes(cfg, st, kind)
+            b = (sum(_call_bytes(cfg, q, kind) for q in stages) if cfg.get("grouped")
+                 else _call_bytes(cfg, st, kind))
             gbs = b / (ms * 1e-3) / 1e9
             srt = sorted(per_call[(si, kind)])
             pick = lambda q: srt[min(len(srt) - 1, int(q * (len(srt) - 1) + 0.5))]  # noqa: E731
@@ -578,7 +596,7 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
             row["checksum"]["grad_input"] = float(st["gx"].double().sum())
         table.append(row)
     dom = max(kind_ms, key=kind_ms.get)
-    launches_dom = len(stages)
+    launches_dom = 1 if cfg.get("grouped") else len(stages)
     achieved = kind_bytes[dom] / (kind_ms[dom] * 1e-3) / 1e9
     share = kind_ms[dom] / sum(kind_ms.values())
     if cfg.get("module") == "full":
@@ -586,7 +604,8 @@ def measure(cfg, ctx, images, steps, warmup, offsets="u2", softmax=False, determ
                  if dom == "bwd" else "full-module forward: tcgen05 linear + module_fwd_kernel + tcgen05 linear")
     else:
         kname = "memset + bwd33_kernel" if dom == "bwd" else (
-            "module_fwd_kernel: tcgen05 linear + aggregation" if cfg.get("module") else "fwd33_kernel")
+            "module_fwd_kernel: tcgen05 linear + aggregation" if cfg.get("module") else
+            "fwd33_group_kernel (all stages)" if cfg.get("grouped") else "fwd33_kernel")
     roofline = {"bound": "hbm", "kernel": f"dcnv4 {dom} ({kname}), {launches_dom} launches per step",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
@@ -844,7 +863,7 @@ def main(argv=None):
         extras = _extras(args, ctx)
     ctx.sampler.stop()
 
-    n_ours = (2 if cfg["backward"] else 1) * len(stages)
+    n_ours = (2 if cfg["backward"] else 1) * (1 if cfg.get("grouped") else len(stages))
     if cfg["backward"] and args.deterministic:
         n_ours += 2 * len(stages)  # per-image maxima + int64 -> T conversion
     elif cfg["backward"] and cfg["dtype"] != "f32":

@@ -54,7 +54,7 @@ extern "C" {
 #define DCNV4_API
 #endif
 
-#define DCNV4_VERSION 120 /* 1.2.0: module path (include/dcnv4_module.h); 1.1.0: dcnv4_params.deterministic */
+#define DCNV4_VERSION 130 /* 1.3.0: dcnv4_forward_grouped, full-module GEMMs (dcnv4_module.h); 1.2.0: module path; 1.1.0: dcnv4_params.deterministic */
 
 typedef enum { DCNV4_F32 = 0, DCNV4_F16 = 1, DCNV4_BF16 = 2 } dcnv4_dtype;
 
@@ -104,6 +104,20 @@ DCNV4_API int dcnv4_output_size(const dcnv4_params *p, int64_t *H_out, int64_t *
  * (y must not alias x or om).  Bit-deterministic.  One kernel launch (none if N = 0). */
 DCNV4_API int dcnv4_forward(const dcnv4_params *p, dcnv4_dtype dtype, const void *input,
                   const void *offset_mask, void *output, void *stream);
+
+/* Several independent forwards in ONE launch (e.g. the four stages of a backbone, or a
+ * batch-1 pyramid whose late stages are too small to fill the GPU on their own):
+ * output i = DCNv4(inputs[i], offset_masks[i]) with params[i], exactly as dcnv4_forward
+ * computes it (bit-identical).  1 <= count <= 8; all problems share dtype.  When every
+ * non-empty problem runs the TMA-halo kernel (3x3, stride 1, dilation 1) with the same
+ * channel layout (D * sizeof(T)) and tile shape, a single persistent grid sweeps the
+ * concatenated tile ranges, so the tail of one problem overlaps the next; otherwise the
+ * problems are launched one after another on `stream`.  Every problem is validated
+ * before anything is launched (errors name the problem index).                        */
+DCNV4_API int dcnv4_forward_grouped(const dcnv4_params *const *params, int32_t count,
+                                    dcnv4_dtype dtype, const void *const *inputs,
+                                    const void *const *offset_masks, void *const *outputs,
+                                    void *stream);
 
 /* Workspace bytes dcnv4_backward needs: 0 for DCNV4_F32; N*H*W*C*4 (an fp32
  * grad_input accumulator) for DCNV4_F16 / DCNV4_BF16; with deterministic = 1, for every

@@ -66,7 +66,11 @@ def lib() -> ctypes.CDLL:
         i32p = ctypes.POINTER(ctypes.c_int32)
         L.dcnv4_launch_info.argtypes = [P, ctypes.c_int, ctypes.c_int, i32p, i32p, i32p, i32p,
                                         ctypes.POINTER(ctypes.c_int64)]
-        for fn in ("dcnv4_output_size", "dcnv4_forward", "dcnv4_backward", "dcnv4_launch_info"):
+        PP = ctypes.POINTER(ctypes.POINTER(Params))
+        VPP = ctypes.POINTER(ctypes.c_void_p)
+        L.dcnv4_forward_grouped.argtypes = [PP, ctypes.c_int32, ctypes.c_int, VPP, VPP, VPP, VP]
+        for fn in ("dcnv4_output_size", "dcnv4_forward", "dcnv4_backward", "dcnv4_launch_info",
+                   "dcnv4_forward_grouped"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -196,6 +200,32 @@ def forward(x: torch.Tensor, offset_mask: torch.Tensor, group: int, kernel_size=
         _check(lib().dcnv4_forward(ctypes.byref(p), DTYPE_CODE[x.dtype], _ptr(x),
                                    _ptr(offset_mask), _ptr(out), ctypes.c_void_p(_stream_ptr(x))))
     return out
+
+
+def forward_grouped(xs, offset_masks, groups, kernel_size=3, stride=1, pad=1, dilation=1,
+                    offset_scale=1.0, softmax=False, outs=None):
+    """[DCNv4(x_i, om_i)] for up to 8 independent problems in one dcnv4_forward_grouped call
+    (one persistent launch when they share the kernel instantiation and tile shape)."""
+    n = len(xs)
+    if not (len(offset_masks) == n and len(groups) == n and 1 <= n <= 8):
+        raise ValueError("xs, offset_masks, groups must have the same length in [1, 8]")
+    _check_tensors(*xs, *offset_masks)
+    ps = [_params_for(x, om, G, kernel_size, stride, pad, dilation, offset_scale, softmax)
+          for x, om, G in zip(xs, offset_masks, groups)]
+    if outs is None:
+        outs = []
+        for x, p in zip(xs, ps):
+            Ho, Wo = output_size(p)
+            outs.append(torch.empty((x.shape[0], Ho, Wo, x.shape[3]), dtype=x.dtype, device=x.device))
+    for x, p, o in zip(xs, ps, outs):
+        Ho, Wo = output_size(p)
+        _check_buffer(o, (x.shape[0], Ho, Wo, x.shape[3]), x, "out")
+    parr = (ctypes.POINTER(Params) * n)(*[ctypes.pointer(p) for p in ps])
+    vp = lambda ts: (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])  # noqa: E731
+    with torch.cuda.device(xs[0].device):
+        _check(lib().dcnv4_forward_grouped(parr, n, DTYPE_CODE[xs[0].dtype], vp(xs), vp(offset_masks), vp(outs),
+                                           ctypes.c_void_p(_stream_ptr(xs[0]))))
+    return outs
 
 
 def workspace_bytes(p: Params, dtype: torch.dtype) -> int:

@@ -312,7 +312,7 @@ bool encode_nhwc_map(int dtype, const void* ptr, int64_t N, int64_t Hh, int64_t 
 // when the geometry, alignment and shared-memory budget allow it; the caller otherwise
 // keeps the global-gather kernel.  `x` may be NULL (planning only, lc->halo stays false).
 bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const void* x,
-                dcnv4::Launch* lc, dcnv4::Geo* g) {
+                dcnv4::Launch* lc, dcnv4::Geo* g, int th_force = 0) {
   const char* path = dcnv4::ablation(dcnv4::kAblFwdPath);
   if (path && path[0] == 'g') return false;
   if (p->kernel_h != 3 || p->kernel_w != 3 || p->stride_h != 1 || p->stride_w != 1 ||
@@ -332,6 +332,7 @@ bool plan_fwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   const char* th_env = dcnv4::ablation(dcnv4::kAblFwd33TH);
   if (th_env && *th_env) TH = std::max(1, std::min(TH, atoi(th_env)));
   if (TH > Ho) TH = (int)Ho;
+  if (th_force) TH = th_force;  // grouped launch: one tile shape for every problem
   const int K = 9;
   const int S = p->om_stride ? p->om_stride : 3 * p->G * K;
   const int segB_raw = GC * 3 * K * b;
@@ -507,7 +508,7 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
 
 int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t Wo,
                 dcnv4::Launch* lc, dcnv4::Geo* g, const void* x = nullptr,
-                const void* gy = nullptr) {
+                const void* gy = nullptr, int th_force = 0) {
   const int b = elem_size(dtype);
   const int nch = p->D * b / 16;
   int cpl = default_cpl(nch, pass);
@@ -555,7 +556,7 @@ int make_launch(const dcnv4_params* p, int dtype, int pass, int64_t Ho, int64_t 
   g->rot_shift = tc.rot_shift;
   g->seg = seg_bytes / b;
   lc->halo = false;
-  if (pass == 0) plan_fwd33(p, dtype, Ho, Wo, x, lc, g);
+  if (pass == 0) plan_fwd33(p, dtype, Ho, Wo, x, lc, g, th_force);
   else plan_bwd33(p, dtype, Ho, Wo, x, gy, lc, g);
   g->tiles_total = (int)lc->ctas;
   lc->persistent = dcnv4::ablation(dcnv4::kAblNonPersistent)[0] != '1';
@@ -648,6 +649,94 @@ int dcnv4_forward(const dcnv4_params* p, dcnv4_dtype dtype, const void* input,
     default: e = dcnv4::launch_fwd_bf16(lc, g, input, offset_mask, output); break;
   }
   if (e != cudaSuccess) return cuda_fail(e, "dcnv4_forward launch");
+  return DCNV4_OK;
+}
+
+static_assert(sizeof(dcnv4::Fwd33Group) <= 32000, "grouped-forward kernel parameters exceed 32 KB");
+
+int dcnv4_forward_grouped(const dcnv4_params* const* params, int32_t count, dcnv4_dtype dtype,
+                          const void* const* inputs, const void* const* offset_masks, void* const* outputs,
+                          void* stream) {
+  g_err[0] = 0;
+  if (count < 1 || count > dcnv4::kMaxGroup)
+    return fail(DCNV4_ERR_INVALID_ARG, "count = %d must be in [1, %d]", count, dcnv4::kMaxGroup);
+  if (!params || !inputs || !offset_masks || !outputs)
+    return fail(DCNV4_ERR_INVALID_ARG, "params/inputs/offset_masks/outputs array is NULL");
+  int64_t Ho[dcnv4::kMaxGroup], Wo[dcnv4::kMaxGroup];
+  for (int i = 0; i < count; ++i) {  // validate every problem before launching anything
+    const dcnv4_params* p = params[i];
+    int rc = validate_geometry(p, dtype, &Ho[i], &Wo[i]);
+    if (rc) {
+      char m[512];
+      snprintf(m, sizeof(m), "problem %d: %s", i, g_err);
+      return fail(rc, "%s", m);
+    }
+    if (p->N == 0) continue;
+    if (!inputs[i] || !offset_masks[i] || !outputs[i])
+      return fail(DCNV4_ERR_INVALID_ARG, "problem %d: input/offset_mask/output is NULL", i);
+    if (!aligned16(inputs[i]) || !aligned16(outputs[i]))
+      return fail(DCNV4_ERR_MISALIGNED, "problem %d: input/output not 16-byte aligned", i);
+    if (reinterpret_cast<uintptr_t>(offset_masks[i]) % elem_size(dtype))
+      return fail(DCNV4_ERR_MISALIGNED, "problem %d: offset_mask is not element aligned", i);
+  }
+  // one launch when every non-empty problem takes the TMA-halo kernel with the same
+  // template instantiation and tile shape; otherwise one dcnv4_forward per problem
+  dcnv4::Fwd33Group grp;
+  grp.count = 0;
+  dcnv4::Launch l0;
+  bool one = true;
+  int th = 0;
+  long long tiles = 0;
+  for (int i = 0; i < count && one; ++i) {
+    const dcnv4_params* p = params[i];
+    if (p->N == 0) continue;
+    dcnv4::Launch lc;
+    dcnv4::Geo g;
+    if (make_launch(p, dtype, 0, Ho[i], Wo[i], &lc, &g, inputs[i], nullptr, th) != DCNV4_OK || !lc.halo) {
+      one = false;
+      break;
+    }
+    if (grp.count == 0) {
+      l0 = lc;
+      th = g.TH;
+      // re-plan the first problem without its own tile-height clamp only if needed below
+    }
+    const dcnv4::Geo& g0 = grp.count ? grp.p[0].g : g;
+    if (lc.nch != l0.nch || lc.cpl != l0.cpl || lc.unit != l0.unit || g.TH != th || g.seg != g0.seg ||
+        g.halo_bytes != g0.halo_bytes || g.rot_shift != g0.rot_shift || lc.threads != l0.threads ||
+        lc.smem != l0.smem) {
+      one = false;
+      break;
+    }
+    dcnv4::Fwd33Prob& q = grp.p[grp.count++];
+    q.xmap = lc.xmap;
+    q.g = g;
+    q.x = inputs[i];
+    q.om = offset_masks[i];
+    q.y = outputs[i];
+    q.t0 = (int)tiles;
+    tiles += lc.ctas;
+  }
+  if (one && tiles >= 0x7fffffffLL) one = false;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!one) {
+    for (int i = 0; i < count; ++i) {
+      const int rc = dcnv4_forward(params[i], dtype, inputs[i], offset_masks[i], outputs[i], stream);
+      if (rc) return rc;
+    }
+    return DCNV4_OK;
+  }
+  if (grp.count == 0) return DCNV4_OK;
+  grp.tiles_total = (int)tiles;
+  l0.ctas = tiles;
+  l0.stream = st;
+  cudaError_t e;
+  switch (dtype) {
+    case DCNV4_F32: e = dcnv4::launch_fwd_group_f32(l0, grp.p[0].g, &grp); break;
+    case DCNV4_F16: e = dcnv4::launch_fwd_group_f16(l0, grp.p[0].g, &grp); break;
+    default: e = dcnv4::launch_fwd_group_bf16(l0, grp.p[0].g, &grp); break;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "dcnv4_forward_grouped launch");
   return DCNV4_OK;
 }
 

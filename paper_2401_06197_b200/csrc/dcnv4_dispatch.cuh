@@ -46,7 +46,7 @@ static cudaError_t fwd_variant(const Launch& lc, const Geo& g, const void* x, co
   const T* op = static_cast<const T*>(om);
   T* yp = static_cast<T*>(y);
   if (lc.halo) {  // 3x3 / stride 1 / dilation 1: TMA halo kernel
-    void (*hk)(const __grid_constant__ CUtensorMap, Geo, const T*, const T*, T*);
+    void (*hk)(const __grid_constant__ Fwd33Prob);
     if (lc.unit) hk = fwd33_kernel<T, NCH, CPL, true>;
     else hk = fwd33_kernel<T, NCH, CPL, false>;
     if (lc.smem > 48 * 1024) {
@@ -54,7 +54,14 @@ static cudaError_t fwd_variant(const Launch& lc, const Geo& g, const void* x, co
                                            (int)lc.smem);
       if (e != cudaSuccess) return e;
     }
-    hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(lc.xmap, g, xp, op, yp);
+    Fwd33Prob prob;
+    prob.xmap = lc.xmap;
+    prob.g = g;
+    prob.x = xp;
+    prob.om = op;
+    prob.y = yp;
+    prob.t0 = 0;
+    hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(prob);
     return cudaGetLastError();
   }
   void (*kern)(Geo, const T*, const T*, T*);
@@ -110,6 +117,21 @@ static cudaError_t bwd_variant(const Launch& lc, const Geo& g, const void* x, co
   return cudaGetLastError();
 }
 
+// Several fwd33 problems in one persistent launch (dcnv4_forward_grouped).
+template <typename T, int NCH, int CPL>
+static cudaError_t fwd_group_variant(const Launch& lc, const Geo&, const void* grp) {
+  void (*hk)(const __grid_constant__ Fwd33Group);
+  if (lc.unit) hk = fwd33_group_kernel<T, NCH, CPL, true>;
+  else hk = fwd33_group_kernel<T, NCH, CPL, false>;
+  if (lc.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
+    if (e != cudaSuccess) return e;
+  }
+  hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(
+      *static_cast<const Fwd33Group*>(grp));
+  return cudaGetLastError();
+}
+
 static inline unsigned flat_blocks(long long n) {
   long long blocks = (n + 255) / 256;
   if (blocks > 148LL * 16) blocks = 148LL * 16;
@@ -140,6 +162,9 @@ static inline unsigned flat_blocks(long long n) {
   cudaError_t launch_bwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x, const void* om, \
                                   const void* gy, void* gxacc, void* gom) {                     \
     DCNV4_TABLE(bwd_variant, T, x, om, gy, gxacc, gom)                                         \
+  }                                                                                             \
+  cudaError_t launch_fwd_group_##SUFFIX(const Launch& lc, const Geo& g, const void* grp) {     \
+    DCNV4_TABLE(fwd_group_variant, T, grp)                                                      \
   }                                                                                             \
   cudaError_t launch_convert_##SUFFIX(const float* src, void* dst, long long nchunk,            \
                                       cudaStream_t stream) {                                    \

@@ -615,11 +615,42 @@ DCNV4_DOT_HALF(__half, "f16")
 DCNV4_DOT_HALF(__nv_bfloat16, "bf16")
 #undef DCNV4_DOT_HALF
 
-template <typename T, int NCH, int CPL, bool UNIT>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 0 : 2) fwd33_kernel(const __grid_constant__ CUtensorMap xmap, Geo g,
-                                                    const T* __restrict__ x,
-                                                    const T* __restrict__ om,
-                                                    T* __restrict__ y) {
+// One fwd33 problem: its TMA map, geometry, tensors and first tile in the launch's tile
+// space.  A launch covers one problem (fwd33_kernel) or several with the same storage
+// type, channel layout and tile shape (fwd33_group_kernel, dcnv4_forward_grouped): the
+// persistent CTAs then sweep the concatenated tile ranges, so the tails of small problems
+// (late stages, batch 1) overlap the next problem instead of idling the SMs.
+struct Fwd33Prob {
+  CUtensorMap xmap;
+  Geo g;
+  const void* x;
+  const void* om;
+  void* y;
+  int t0;  // first tile of this problem
+};
+constexpr int kMaxGroup = 8;
+struct Fwd33Group {
+  Fwd33Prob p[kMaxGroup];
+  int count;
+  int tiles_total;
+};
+
+// Problem owning global tile t (count <= kMaxGroup, ranges ascending)
+template <typename Src>
+__device__ __forceinline__ int find_prob(const Src& src, int t) {
+  int pi = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxGroup; ++i)
+    if (i < src.count() && t >= src.prob(i).t0) pi = i;
+  return pi;
+}
+
+// fwd33 body over a problem source: src.count(), src.prob(i) -> const Fwd33Prob&,
+// src.tiles_total().  Fields used uniformly (TH, halo sizes, seg, rot_shift, softmax, s)
+// are equal across the problems of one launch (checked on the host).
+template <typename T, int NCH, int CPL, bool UNIT, typename Src>
+__device__ __forceinline__ void fwd33_body(const Src& src) {
+  const Geo& g = src.prob(0).g;  // uniform fields
   // Specialised for the paper's grid (3x3, stride 1, dilation 1; any padding):
   //   TW = 8 output columns, GC groups per CTA so one halo pixel is PB = GC*D*b >= 128 B,
   //   halo = (TH + 6) x 14 pixels, all strides compile-time (shift/immediate addressing).
@@ -656,26 +687,32 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 0 : 2) fwd33_kernel(cons
     co[h] = (((h + rot) & (CPL - 1)) * L + lg) * E;
     hb0[h] = smem_u32(smem) + (uint32_t)(gl * NCH * 16 + co[h] * (int)sizeof(T));
   }
-  const int H = g.H, W = g.W, C = g.C;
   const float s = g.s;
   const unsigned segB = (unsigned)g.seg * sizeof(T);
 
-  auto decode = [&](int t, int& n, int& h0, int& w0, int& g0) {
-    const unsigned q1 = fdiv((unsigned)t, g.fd_gb);
-    g0 = (t - (int)q1 * g.gblocks) * GC;
-    const unsigned q2 = fdiv(q1, g.fd_tw);
-    w0 = ((int)q1 - (int)q2 * g.tiles_w) * TW;
-    const unsigned q3 = fdiv(q2, g.fd_th);
-    h0 = ((int)q2 - (int)q3 * g.tiles_h) * TH;
+  // global tile -> (problem, image, tile origin, group block)
+  auto decode = [&](int t, int& pi, int& n, int& h0, int& w0, int& g0) {
+    pi = find_prob(src, t);
+    const Geo& q = src.prob(pi).g;
+    t -= src.prob(pi).t0;
+    const unsigned q1 = fdiv((unsigned)t, q.fd_gb);
+    g0 = (t - (int)q1 * q.gblocks) * GC;
+    const unsigned q2 = fdiv(q1, q.fd_tw);
+    w0 = ((int)q1 - (int)q2 * q.tiles_w) * TW;
+    const unsigned q3 = fdiv(q2, q.fd_th);
+    h0 = ((int)q2 - (int)q3 * q.tiles_h) * TH;
     n = (int)q3;
   };
   auto issue = [&](int t, int b) {
-    int n, h0, w0, g0;
-    decode(t, n, h0, w0, g0);
+    int pi, n, h0, w0, g0;
+    decode(t, pi, n, h0, w0, g0);
+    const Fwd33Prob& P = src.prob(pi);
+    const Geo& g = P.g;
+    const T* om = static_cast<const T*>(P.om);
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bar[b], (uint32_t)g.halo_box_bytes);
-      tma_load_4d(smem + b * g.halo_bytes, &xmap, g0 * g.D, w0 - g.pw - 2, h0 - g.ph - 2, n, &bar[b]);
+      tma_load_4d(smem + b * g.halo_bytes, &P.xmap, g0 * g.D, w0 - g.pw - 2, h0 - g.ph - 2, n, &bar[b]);
     }
     // offset_mask: GC*3K values per tile pixel, as upp units of g.unit bytes
     const char* src0 = reinterpret_cast<const char*>(
@@ -694,19 +731,25 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 0 : 2) fwd33_kernel(cons
     }
   };
 
+  const int tiles_total = src.tiles_total();
   int t = blockIdx.x;
   issue(t, 0);
   cp_async_commit();
-  for (int it = 0; t < g.tiles_total; t += gridDim.x, ++it) {
+  for (int it = 0; t < tiles_total; t += gridDim.x, ++it) {
     const int b = it & 1;
     const int tn = t + gridDim.x;
-    if (tn < g.tiles_total) issue(tn, b ^ 1);
+    if (tn < tiles_total) issue(tn, b ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
     mbar_wait(&bar[b], (uint32_t)((it >> 1) & 1));
     __syncthreads();
-    int n, h0, w0, g0;
-    decode(t, n, h0, w0, g0);
+    int pi, n, h0, w0, g0;
+    decode(t, pi, n, h0, w0, g0);
+    const Fwd33Prob& P = src.prob(pi);
+    const Geo& g = P.g;
+    const T* x = static_cast<const T*>(P.x);
+    T* y = static_cast<T*>(P.y);
+    const int H = g.H, W = g.W, C = g.C;
     const int ho = h0 + py, wo = w0 + px;
     if (slot_ok && ho < g.Ho && wo < g.Wo) {
       const T* row = ombase + b * npix * g.seg + (py * TW + px) * g.seg + gl * 3 * K;
@@ -796,6 +839,28 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 0 : 2) fwd33_kernel(cons
     __syncthreads();  // everyone is done with halo[b] / om[b] before they are refilled
   }
   cp_async_wait<0>();
+}
+
+template <typename T, int NCH, int CPL, bool UNIT>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 0 : 2) fwd33_kernel(const __grid_constant__ Fwd33Prob prob) {
+  struct One {
+    const Fwd33Prob& p;
+    __device__ int count() const { return 1; }
+    __device__ const Fwd33Prob& prob(int) const { return p; }
+    __device__ int tiles_total() const { return p.g.tiles_total; }
+  } src{prob};
+  fwd33_body<T, NCH, CPL, UNIT>(src);
+}
+
+template <typename T, int NCH, int CPL, bool UNIT>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 0 : 2) fwd33_group_kernel(const __grid_constant__ Fwd33Group grp) {
+  struct Many {
+    const Fwd33Group& q;
+    __device__ int count() const { return q.count; }
+    __device__ const Fwd33Prob& prob(int i) const { return q.p[i]; }
+    __device__ int tiles_total() const { return q.tiles_total; }
+  } src{grp};
+  fwd33_body<T, NCH, CPL, UNIT>(src);
 }
 
 // ------------------------------------------------------------------ backward

@@ -32,6 +32,8 @@ struct Launch {
                                   const void* om, void* y);                                \
   cudaError_t launch_bwd_##SUFFIX(const Launch& lc, const Geo& g, const void* x,          \
                                   const void* om, const void* gy, void* gxacc, void* gom); \
+  cudaError_t launch_fwd_group_##SUFFIX(const Launch& lc, const Geo& g,                    \
+                                        const void* grp /* Fwd33Group */);                 \
   cudaError_t launch_convert_##SUFFIX(const float* src, void* dst, long long nchunk,      \
                                       cudaStream_t stream);                                \
   cudaError_t launch_detmax_##SUFFIX(const void* gy, const void* om, long long N, int npix, \

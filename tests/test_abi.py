@@ -108,7 +108,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(b.LIB_PATH)
     for name in _declared():
         assert hasattr(lib, name), name
-    assert pkg.lib().dcnv4_version() == 120
+    assert pkg.lib().dcnv4_version() == 130
 
 
 def test_params_struct_layout():
