@@ -90,10 +90,13 @@ DCNV4_API int dcnv4_module_core_forward(const dcnv4_params *p, dcnv4_dtype dtype
 
 /* ------------------------------------------------------------------------------------
  * Dense layers of the full module and their backward (tcgen05 GEMMs, csrc/gemm.cu).
- * All three take row-major T matrices (F16/BF16 only; F32 -> UNSUPPORTED), fp32
- * accumulation in tensor memory, one persistent launch (+ the small launches noted);
- * every pointer 16-B aligned (bias / grad_bias 2-B) else MISALIGNED; every channel count
- * and leading dimension a multiple of 8 (16-B rows) else UNSUPPORTED; M < 2^31.
+ * All three take row-major T matrices, fp32 accumulation in tensor memory, one
+ * persistent launch (+ the small launches noted).  F16/BF16: kind::f16 MMAs.  F32: 3xTF32
+ * on kind::tf32 (each operand split into an exact tf32 high part and its remainder;
+ * hi.hi + hi.lo + lo.hi, relative error ~2^-20 per product, within the fp32 parity bar).
+ * Every pointer 16-B aligned (bias / grad_bias element-aligned) else MISALIGNED; every
+ * channel count and leading dimension a multiple of 16 B (8 halves / 4 floats) else
+ * UNSUPPORTED; M < 2^31.
  * Bit-deterministic except dcnv4_linear_grad_weight (fp32 reductions over K splits).    */
 
 /* y[M][N] = RN_T(x[M][K] . weight[N][K]^T + bias[N])  (nn.Linear layout; the module's

@@ -37,15 +37,37 @@ def _source_hash() -> str:
 STAMP = os.path.join(BUILD, "libdcnv4.sha256")
 
 
+def _object_hash(src: str) -> str:
+    """sha256 of one translation unit: its source, every header it may include, the flags."""
+    h = hashlib.sha256()
+    with open(os.path.join(CSRC, src), "rb") as fh:
+        h.update(fh.read())
+    hdrs = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
+    hdrs += [os.path.join(os.path.dirname(HERE), "include", n) for n in ("dcnv4.h", "msda.h", "dcnv4_module.h")]
+    for f in hdrs:
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join([NVCC, *ARCH, *FLAGS]).encode())
+    return h.hexdigest()
+
+
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, src.replace(".cu", ".o"))
     log = os.path.join(BUILD, src.replace(".cu", ".ptxas.log"))
+    stamp = obj + ".sha256"
+    digest = _object_hash(src)
+    if os.path.exists(obj) and os.path.exists(stamp):
+        with open(stamp) as f:
+            if f.read().strip() == digest:
+                return obj  # unchanged translation unit
     cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
     if r.returncode:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
+    with open(stamp, "w") as f:
+        f.write(digest + "\n")
     return obj
 
 

@@ -166,21 +166,23 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return enc;
 }
 
-// 2-D row-major [rows][cols] half tensor, box {box_c, box_r}, 128-B swizzle, zero fill
+// 2-D row-major [rows][cols] tensor of T (fp16 / bf16 / fp32 by dtype), box {box_c, box_r},
+// 128-B swizzle, zero fill
 inline CUresult encode2d(CUtensorMap* map, int dtype, const void* ptr, long long rows, long long cols,
-                  int box_c, int box_r) {
+                  int box_c, int box_r, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = encoder();
   if (!enc) return CUDA_ERROR_NOT_SUPPORTED;
+  const cuuint64_t eb = dtype == DCNV4_F32 ? 4 : 2;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * eb};
   const cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
   const cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapDataType dt =
-      dtype == DCNV4_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUtensorMapDataType dt = dtype == DCNV4_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : dtype == DCNV4_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                      : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   auto run = [&] {
     return enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+               swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   };
   CUresult r = run();
   if (r == CUDA_ERROR_INVALID_CONTEXT) {  // thread without a current context (autograd worker)

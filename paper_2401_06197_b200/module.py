@@ -237,10 +237,17 @@ FULL_KEYS = ("w_in", "b_in", "w_om", "b_om", "w_out", "b_out")
 
 def full_forward(x: torch.Tensor, params: dict, group: int, offset_scale=1.0, softmax=False):
     """Full DCNv4 module forward (R22): v = linear(x; W_in), a = DCNv4(v, linear(x; W_om))
-    fused in one kernel, y = linear(a; W_out).  Three launches.  Returns (y, (v, a)) --
+    fused in one kernel (f16/bf16; fp32: offset_mask linear + dcnv4_forward), y =
+    linear(a; W_out).  Three launches (fp32: four).  Returns (y, (v, a)) --
     the saved activations of full_backward (the offset_mask is recomputed there)."""
     v = linear(x, params["w_in"], params.get("b_in"))
-    a = core_forward(x, v, params["w_om"], params.get("b_om"), group, offset_scale, softmax)
+    if x.dtype == torch.float32:
+        # fp32: 3xTF32 GEMMs (csrc/gemm.cu) and the fp32 operator; the offset_mask goes
+        # through memory (the fused kernel's tensor-core linear is f16/bf16)
+        om = linear(x, params["w_om"], params.get("b_om"))
+        a = dcnv4_forward(v, om, group, 3, 1, 1, 1, offset_scale, softmax)
+    else:
+        a = core_forward(x, v, params["w_om"], params.get("b_om"), group, offset_scale, softmax)
     y = linear(a, params["w_out"], params.get("b_out"))
     return y, (v, a)
 
@@ -256,8 +263,10 @@ def full_backward(x: torch.Tensor, params: dict, group: int, gy: torch.Tensor, s
     g = {}
     g["w_out"], g["b_out"] = linear_grad_weight(a, gy, with_bias=params.get("b_out") is not None)
     ga = linear_grad_input(gy, params["w_out"])
-    S = om_stride_for(group)
-    om = offset_mask_linear(x, params["w_om"], params.get("b_om"), group, S)
+    if x.dtype == torch.float32:
+        om = linear(x, params["w_om"], params.get("b_om"))  # [.., 3GK], S = 3GK
+    else:
+        om = offset_mask_linear(x, params["w_om"], params.get("b_om"), group, om_stride_for(group))
     gv, gom = dcnv4_backward(v, om, ga, group, 3, 1, 1, 1, offset_scale, softmax)
     J = params["w_om"].shape[0]
     g["x"] = linear_grad_input(gom, params["w_om"], J, gv, params["w_in"])

@@ -19,7 +19,7 @@ import paper_2401_06197_b200 as pkg
 from paper_2401_06197_b200 import module as mod
 
 pytestmark = pytest.mark.gpu
-TDT = {"f16": torch.float16, "bf16": torch.bfloat16}
+TDT = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}
 TOL = 1e-2
 
 
@@ -188,3 +188,52 @@ def test_nn_module_autograd_matches_full_backward():
     for k in mod.FULL_KEYS:
         assert torch.isfinite(getattr(m, k).grad.float()).all()
         assert close(getattr(m, k).grad, g[k]), k
+
+
+# ---------------------------------------------------------------- fp32: 3xTF32 GEMMs
+@pytest.mark.parametrize("M,K,N", [(1000, 64, 64), (4133, 72, 136), (257, 512, 320)])
+def test_linear_f32_3xtf32(M, K, N):
+    """fp32 linear on the tf32 tensor cores as 3xTF32 meets the fp32 bar (1e-5)."""
+    dev = torch.device("cuda:0")
+    x = _rand((M, K), "f32", 11)
+    w = _rand((N, K), "f32", 12, K ** -0.5)
+    b = _rand((N,), "f32", 13)
+    y = mod.linear(x.to(dev), w.to(dev), b.to(dev))
+    torch.cuda.synchronize()
+    ref = oracle.linear(x, w, b)
+    assert _err(y, ref, oracle.linear_abs(np.abs(_f(x)), w, b)) <= 1e-5
+
+
+def test_linear_grads_f32_3xtf32():
+    dev = torch.device("cuda:0")
+    M, K, N0, N1 = 3000, 64, 108, 64
+    gy0, w0 = _rand((M, N0), "f32", 14), _rand((N0, K), "f32", 15, N0 ** -0.5)
+    gy1, w1 = _rand((M, N1), "f32", 16), _rand((N1, K), "f32", 17, N1 ** -0.5)
+    gx = mod.linear_grad_input(gy0.to(dev), w0.to(dev), N0, gy1.to(dev), w1.to(dev))
+    x = _rand((M, K), "f32", 18)
+    gw, gb = mod.linear_grad_weight(x.to(dev), gy0.to(dev), N0)
+    torch.cuda.synchronize()
+    ref = _f(gy0) @ _f(w0) + _f(gy1) @ _f(w1)
+    assert _err(gx, ref, np.abs(_f(gy0)) @ np.abs(_f(w0)) + np.abs(_f(gy1)) @ np.abs(_f(w1))) <= 1e-5
+    assert _err(gw, _f(gy0).T @ _f(x), np.abs(_f(gy0)).T @ np.abs(_f(x))) <= 1e-5
+    assert _err(gb, _f(gy0).sum(0), np.abs(_f(gy0)).sum(0)) <= 1e-5
+
+
+def test_full_module_f32():
+    dev = torch.device("cuda:0")
+    N, H, W, G, D = 2, 12, 12, 4, 16
+    x, p = _module_case(N, H, W, G, D, "f32", 70)
+    gy = _rand(x.shape, "f32", 71)
+    xd, pd = x.to(dev), {k: v.to(dev) for k, v in p.items()}
+    y, saved = mod.full_forward(xd, pd, G)
+    g = mod.full_backward(xd, pd, G, gy.to(dev), saved)
+    torch.cuda.synchronize()
+    geo = oracle.Geometry(N=N, H=H, W=W, G=G, D=D)
+    fw = oracle.module_full_forward(geo, x, p, "f32", with_abs=True)
+    assert _err(y, fw["y"], fw["y_abs"]) <= 1e-5
+    bw = oracle.module_full_backward(geo, x, p, gy, "f32")
+    R, C = N * H * W, G * D
+    # scales: |terms| summed like each product (chained magnitudes of the inputs)
+    xf, gyf = np.abs(_f(x).reshape(R, C)), np.abs(_f(gy).reshape(R, C))
+    assert np.abs(_f(g["w_out"]) - bw["w_out"]).max() <= 1e-5 * (gyf.T @ np.abs(fw["a"].reshape(R, C))).max()
+    assert np.abs(_f(g["x"]) - bw["x"]).max() <= 1e-4 * np.abs(bw["x"]).max()
