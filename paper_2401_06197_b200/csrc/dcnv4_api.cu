@@ -401,7 +401,9 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   const int DG = p->D;
   const int PB = GC * DG * b;
   const int per_row = 8 * GC * L;
-  int TH = 256 / per_row;
+  // fp32: 224-thread tiles (TH = 7 at 32 threads per tile row) whose shared memory (5-B bin
+  // entries) and registers fit three CTAs per SM; fp16/bf16: 256 threads, two CTAs
+  int TH = (b == 4 ? 224 : 256) / per_row;
   if (TH < 1) return false;
   const char* th_env = dcnv4::ablation(dcnv4::kAblBwd33TH);
   if (th_env && *th_env) TH = std::max(1, std::min(TH, atoi(th_env)));
@@ -435,8 +437,10 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   const int o_slot = (int)o;
   o = up(o + (size_t)GC * NT * 4, 16);  // fill pointers
   const int o_ent = (int)o;
-  // bin entries: 8 B {a, src} for fp32, 4 B {a in T, src} for half (+ one pad slot per bin)
-  o = up(o + ((size_t)GC * npix * 36 + (size_t)GC * NT) * (b == 4 ? 8 : 4), 16);
+  // bin entries (+ one pad slot per bin): fp32 5 B {a fp32} + {src u8} in two arrays,
+  // half 4 B {a in T | src << 16}
+  const size_t ent_cap = (size_t)GC * npix * 36 + (size_t)GC * NT;
+  o = up(o + ent_cap * (b == 4 ? 5 : 4), 16);
   const int o_wsum = (int)o;
   o = up(o + 33 * 4, 16);
   const int o_bar = (int)o;
@@ -465,6 +469,7 @@ bool plan_bwd33(const dcnv4_params* p, int dtype, int64_t Ho, int64_t Wo, const 
   g2.gy_box_bytes = gy_box;
   g2.o_gy = o_gy; g2.o_om = o_om; g2.o_gom = o_gom; g2.o_cnt = o_cnt; g2.o_slot = o_slot;
   g2.o_ent = o_ent; g2.o_wsum = o_wsum; g2.o_bar = o_bar;
+  g2.ent_cap = (int)ent_cap;
   {  // P4 bin order: expected entry count for U(-2,2)-like offsets, separable in y and x.
     // A sample of output row py lands (floor) on halo row py + j + 2 + floor(dy), j in
     // {0,1,2}, floor(dy) in {-2..1}; its corners cover that row and the next.

@@ -94,6 +94,8 @@ static cudaError_t bwd_variant(const Launch& lc, const Geo& g, const void* x, co
                                            (int)lc.smem);
       if (e != cudaSuccess) return e;
     }
+    // the largest shared-memory carveout, so the occupancy the tile was sized for is reached
+    cudaFuncSetAttribute(hk, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(lc.xmap, lc.gymap, g, xp,
                                                                             op, gxacc, gomp);
     return cudaGetLastError();

@@ -66,6 +66,7 @@ struct Geo {
   // deterministic grad_input (params.deterministic): ceil(log2(Ho*Wo*K)) and the
   // per-image maxima {max|gy|, max|m|} (float bits) written by det_scale_kernel
   int det_lc;
+  int ent_cap;  // bwd33: bin-entry capacity of the tile (fp32 keeps a and src in two arrays)
   const unsigned* detmax;
   // bwd33 P4: halo bins in descending order of their expected entry count (so the lanes of
   // a warp get bins of similar size and wait less on each other); identity if disabled
@@ -1116,7 +1117,7 @@ __device__ __forceinline__ int block_exclusive_scan(int* data, int n, int* warp_
 }
 
 template <typename T, int NCH, int CPL, bool UNIT, bool DET>
-__global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUtensorMap xmap,
+__global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3 : 2) bwd33_kernel(const __grid_constant__ CUtensorMap xmap,
                                                     const __grid_constant__ CUtensorMap gymap, Geo g,
                                                     const T* __restrict__ x,
                                                     const T* __restrict__ om,
@@ -1141,10 +1142,12 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
   int* const fill = reinterpret_cast<int*>(smem + g.o_slot);  // per-bin fill pointers (P3)
   // bin entries (a, source pixel): fp32 -> 8 B {a, src}; fp16/bf16 -> 4 B {a rounded to T |
   // src << 16} (the pull's FHFMA rounds a to T anyway, fma_chunk), half the shared memory
+  // fp32: 5 B per entry in two arrays, a (fp32) and the source pixel (u8), so the tile fits
+  // three CTAs per SM
   constexpr bool ENT8 = sizeof(T) == 4;
-  using Ent = typename std::conditional<ENT8, uint2, uint32_t>::type;
-  using EntPair = typename std::conditional<ENT8, uint4, uint2>::type;
-  Ent* const ent = reinterpret_cast<Ent*>(smem + g.o_ent);
+  uint32_t* const ent = reinterpret_cast<uint32_t*>(smem + g.o_ent);   // half: {a_T | src << 16}
+  float* const ent_a = reinterpret_cast<float*>(smem + g.o_ent);        // fp32: a
+  unsigned char* const ent_s = reinterpret_cast<unsigned char*>(smem + g.o_ent) + 4 * g.ent_cap;  // fp32: src
   int* const wsum = reinterpret_cast<int*>(smem + g.o_wsum);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + g.o_bar);
   if (threadIdx.x == 0) {
@@ -1359,8 +1362,12 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           if (lg < 4 && q < 4 && pick4(P.ok, q) && a != 0.f) {
             const int tt = (P.yl + (q >> 1)) * HWC + P.xl + (q & 1);
             const int e = atomicAdd(&fill[gl * NT + tt], 1);
-            if constexpr (ENT8) ent[e] = make_uint2(__float_as_uint(a), (unsigned)(py * TW + px));
-            else ent[e] = (uint32_t)Elem<T>::bits(a) | ((uint32_t)(py * TW + px) << 16);
+            if constexpr (ENT8) {
+              ent_a[e] = a;
+              ent_s[e] = (unsigned char)(py * TW + px);
+            } else {
+              ent[e] = (uint32_t)Elem<T>::bits(a) | ((uint32_t)(py * TW + px) << 16);
+            }
           }
         }
       }
@@ -1475,14 +1482,19 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
         const int np = ((offs[gg * NT + tt + 1] & ~1) - b0) >> 1;  // entry pairs (last may be half)
         if (np == 0) continue;
         const bool odd = o0 & 1;
-        const EntPair* b = reinterpret_cast<const EntPair*>(ent + b0);
+        const uint2* bh = reinterpret_cast<const uint2*>(ent + b0);       // half: entry pairs
+        const float2* ba = reinterpret_cast<const float2*>(ent_a + b0);   // fp32: weight pairs
+        const unsigned short* bs = reinterpret_cast<const unsigned short*>(ent_s + b0);  // fp32: source pairs
         // decoded entry pair: weights and source pixels
         struct Dec { float a0, a1; unsigned s0, s1; };
-        auto dec = [&](const EntPair& en) {
+        auto dec = [&](int q) {
           Dec d;
           if constexpr (ENT8) {
-            d.a0 = __uint_as_float(en.x); d.s0 = en.y; d.a1 = __uint_as_float(en.z); d.s1 = en.w;
+            const float2 a2 = ba[q];
+            const unsigned s2 = bs[q];
+            d.a0 = a2.x; d.s0 = s2 & 0xffu; d.a1 = a2.y; d.s1 = s2 >> 8;
           } else {
+            const uint2 en = bh[q];
             d.a0 = Elem<T>::from_bits((unsigned short)(en.x & 0xffffu)); d.s0 = en.x >> 16;
             d.a1 = Elem<T>::from_bits((unsigned short)(en.y & 0xffffu)); d.s1 = en.y >> 16;
           }
@@ -1499,7 +1511,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
 #pragma unroll
           for (int e = 0; e < PC * E; ++e) acc[e] = 0;
           for (int q = 0; q < np; ++q) {
-            const Dec en = dec(b[q]);
+            const Dec en = dec(q);
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
               if (r == 1 && odd && q == np - 1) break;
@@ -1527,7 +1539,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
           // are in flight together), then the last pair
 #pragma unroll 4
           for (int q = 0; q < np - 1; ++q) {
-            const Dec en = dec(b[q]);
+            const Dec en = dec(q);
             const T* src0 = gyg + en.s0 * (GC * DG);
             const T* src1 = gyg + en.s1 * (GC * DG);
 #pragma unroll
@@ -1537,7 +1549,7 @@ __global__ void __launch_bounds__(256) bwd33_kernel(const __grid_constant__ CUte
             }
           }
           {
-            const Dec en = dec(b[np - 1]);
+            const Dec en = dec(np - 1);
             const T* src0 = gyg + en.s0 * (GC * DG);
             const T* src1 = gyg + (odd ? 0u : en.s1) * (GC * DG);
             const float a1 = odd ? 0.f : en.a1;
