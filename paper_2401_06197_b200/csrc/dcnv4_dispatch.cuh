@@ -54,6 +54,7 @@ static cudaError_t fwd_variant(const Launch& lc, const Geo& g, const void* x, co
                                            (int)lc.smem);
       if (e != cudaSuccess) return e;
     }
+    cudaFuncSetAttribute(hk, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     Fwd33Prob prob;
     prob.xmap = lc.xmap;
     prob.g = g;
@@ -129,6 +130,7 @@ static cudaError_t fwd_group_variant(const Launch& lc, const Geo&, const void* g
     cudaError_t e = cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
     if (e != cudaSuccess) return e;
   }
+  cudaFuncSetAttribute(hk, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   hk<<<grid_size(lc, (const void*)hk), lc.threads, lc.smem, lc.stream>>>(
       *static_cast<const Fwd33Group*>(grp));
   return cudaGetLastError();
