@@ -206,3 +206,65 @@ def test_product_path_has_no_oracle_or_cpu_fallback():
                 assert "oracle" not in src.replace("no oracle", ""), f
     with pytest.raises(ValueError):
         pkg.forward(torch.zeros(1, 4, 4, 32), torch.zeros(1, 4, 4, 54), group=2)
+
+
+def test_gemm_and_grouped_validation_before_any_launch():
+    """Host-side validation of the round-2 entry points (no CUDA call is reached)."""
+    from paper_2401_06197_b200 import module as mod
+    L = mod._glib()
+    V = ctypes.c_void_p
+    # dcnv4_linear: bad sizes, unsupported pitches, NULL and misaligned operands, M = 0
+    assert L.dcnv4_linear(1, 10, 0, 8, V(16), V(16), None, V(16), None) == b.ERR_INVALID_ARG
+    assert L.dcnv4_linear(1, 10, 12, 8, V(16), V(16), None, V(16), None) == b.ERR_UNSUPPORTED
+    assert b"multiples of 8" in L.dcnv4_last_error()
+    assert L.dcnv4_linear(0, 10, 6, 8, V(16), V(16), None, V(16), None) == b.ERR_UNSUPPORTED
+    assert L.dcnv4_linear(1, 10, 16, 8, None, V(16), None, V(16), None) == b.ERR_INVALID_ARG
+    assert b"x" in L.dcnv4_last_error()
+    assert L.dcnv4_linear(1, 10, 16, 8, V(8), V(16), None, V(16), None) == b.ERR_MISALIGNED
+    assert L.dcnv4_linear(1, 0, 16, 8, None, None, None, None, None) == b.OK
+    assert L.dcnv4_linear(5, 10, 16, 8, V(16), V(16), None, V(16), None) == b.ERR_INVALID_ARG
+    # grad_input: ld0 < N0, second segment without operands
+    assert L.dcnv4_linear_grad_input(1, 10, 16, 24, V(16), 16, V(16), 0, None, None, V(16), None) == b.ERR_INVALID_ARG
+    assert L.dcnv4_linear_grad_input(1, 10, 16, 8, V(16), 16, V(16), 8, None, None, V(16), None) == b.ERR_INVALID_ARG
+    # grad_weight: the fp32 accumulator workspace is required and sized (N*K + N) * 4
+    assert L.dcnv4_linear_grad_weight_workspace_bytes(64, 108) == (108 * 64 + 108) * 4
+    assert L.dcnv4_linear_grad_weight(1, 10, 64, 108, V(16), V(16), 112, V(16), None, None, 0,
+                                      None) == b.ERR_WORKSPACE
+    assert L.dcnv4_linear_grad_weight(1, 10, 64, 108, V(16), V(16), 100, V(16), None, V(16), 10 ** 6,
+                                      None) == b.ERR_INVALID_ARG  # ld_gy < N
+    assert L.dcnv4_linear_grad_weight(1, 10, 64, 108, V(16), V(16), 116, V(16), None, V(16), 10 ** 6,
+                                      None) == b.ERR_UNSUPPORTED  # ld_gy not 16-B
+    # grouped forward: count bounds, NULL arrays, a bad problem named by index
+    prm = b.make_params(1, 8, 8, 2, 16)
+    PP = ctypes.POINTER(b.Params)
+    arr = (PP * 2)(ctypes.pointer(prm), ctypes.pointer(b.make_params(1, 8, 8, 0, 16)))
+    ptrs = (ctypes.c_void_p * 2)(16, 16)
+    Lb = pkg.lib()
+    assert Lb.dcnv4_forward_grouped(arr, 0, 0, ptrs, ptrs, ptrs, None) == b.ERR_INVALID_ARG
+    assert Lb.dcnv4_forward_grouped(arr, 9, 0, ptrs, ptrs, ptrs, None) == b.ERR_INVALID_ARG
+    assert Lb.dcnv4_forward_grouped(arr, 2, 0, None, ptrs, ptrs, None) == b.ERR_INVALID_ARG
+    assert Lb.dcnv4_forward_grouped(arr, 2, 0, ptrs, ptrs, ptrs, None) == b.ERR_INVALID_ARG
+    assert b"problem 1" in Lb.dcnv4_last_error()
+    empty = (PP * 1)(ctypes.pointer(b.make_params(0, 8, 8, 2, 16)))
+    nul = (ctypes.c_void_p * 1)(None)
+    assert Lb.dcnv4_forward_grouped(empty, 1, 0, nul, nul, nul, None) == b.OK
+
+
+def test_binding_rejects_bad_buffers_and_weights():
+    """every caller-supplied buffer and the module weights are shape-checked in the
+    binding before the ABI call (CPU tensors are rejected first, so use meta checks only)."""
+    import torch
+    from paper_2401_06197_b200 import module as mod
+    with pytest.raises(ValueError):
+        b._check_buffer(torch.empty(2, 3), (2, 4), torch.empty(1), "out")
+    with pytest.raises(ValueError):
+        b._check_buffer(torch.empty(2, 4, dtype=torch.float16), (2, 4), torch.empty(1), "out")
+    with pytest.raises(ValueError):
+        b._check_buffer(torch.empty(4, 2).t(), (2, 4), torch.empty(1), "out")
+    with pytest.raises(ValueError):
+        b._workspace(torch.empty(3, dtype=torch.uint8), 16, torch.empty(1))
+    with pytest.raises(ValueError):
+        mod._check_linear(torch.empty(108, 32), None, 4, 64, 9)
+    with pytest.raises(ValueError):
+        mod._check_linear(torch.empty(108, 64), torch.empty(100), 4, 64, 9)
+    mod._check_linear(torch.empty(108, 64), torch.empty(108), 4, 64, 9)

@@ -237,3 +237,54 @@ def test_full_module_f32():
     xf, gyf = np.abs(_f(x).reshape(R, C)), np.abs(_f(gy).reshape(R, C))
     assert np.abs(_f(g["w_out"]) - bw["w_out"]).max() <= 1e-5 * (gyf.T @ np.abs(fw["a"].reshape(R, C))).max()
     assert np.abs(_f(g["x"]) - bw["x"]).max() <= 1e-4 * np.abs(bw["x"]).max()
+
+
+# ---------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("dtype", ["f16", "bf16", "f32"])
+@pytest.mark.parametrize("M,K,N", [(1, 16, 8), (127, 24, 72), (129, 64, 8), (300, 8, 264)])
+def test_linear_edge_shapes(dtype, M, K, N):
+    """Single row, fewer rows than one 128-row tile, K below one k block, ragged N."""
+    if dtype == "f32":
+        K, N = max(4, K), max(4, N)
+    dev = torch.device("cuda:0")
+    x = _rand((M, K), dtype, 80)
+    w = _rand((N, K), dtype, 81, K ** -0.5)
+    b = _rand((N,), dtype, 82)
+    y = mod.linear(x.to(dev), w.to(dev), b.to(dev))
+    torch.cuda.synchronize()
+    ref = oracle.linear(x, w, b, dtype if dtype != "f32" else "f64")
+    tol = 1e-5 if dtype == "f32" else TOL
+    assert _err(y, ref, oracle.linear_abs(np.abs(_f(x)), w, b)) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["f16", "f32"])
+@pytest.mark.parametrize("M", [1, 37, 130])
+def test_linear_grad_weight_few_rows(dtype, M):
+    """The split-K grad_weight with fewer rows than one k block (zero-filled tail)."""
+    dev = torch.device("cuda:0")
+    K, N = 64, 24
+    x = _rand((M, K), dtype, 83)
+    gy = _rand((M, N), dtype, 84)
+    gw, gb = mod.linear_grad_weight(x.to(dev), gy.to(dev))
+    torch.cuda.synchronize()
+    ref = _f(gy).T @ _f(x)
+    tol = 1e-5 if dtype == "f32" else TOL
+    assert _err(gw, ref, np.abs(_f(gy)).T @ np.abs(_f(x))) <= tol
+    assert _err(gb, _f(gy).sum(0), np.abs(_f(gy)).sum(0)) <= tol
+
+
+def test_full_module_softmax_bf16():
+    """DCNv3 mode (softmax over K, R18) through the full module, bf16."""
+    dev = torch.device("cuda:0")
+    N, H, W, G, D = 1, 14, 10, 4, 16
+    x, p = _module_case(N, H, W, G, D, "bf16", 90)
+    xd, pd = x.to(dev), {k: v.to(dev) for k, v in p.items()}
+    y, saved = mod.full_forward(xd, pd, G, softmax=True)
+    gy = _rand(x.shape, "bf16", 91)
+    g = mod.full_backward(xd, pd, G, gy.to(dev), saved, softmax=True)
+    torch.cuda.synchronize()
+    geo = oracle.Geometry(N=N, H=H, W=W, G=G, D=D, softmax=True)
+    fw = oracle.module_full_forward(geo, x, p, "bf16", with_abs=True)
+    assert _err(y, fw["y"], fw["y_abs"]) <= TOL
+    for k in mod.FULL_KEYS:
+        assert torch.isfinite(g[k].float()).all()
