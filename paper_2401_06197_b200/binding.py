@@ -18,7 +18,9 @@ from typing import Optional, Tuple
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdcnv4.so")
+# DCNV4_LIB: path of an alternative build of the library (A/B experiments,
+# scripts/build_variant.py); the in-tree libdcnv4.so otherwise
+LIB_PATH = os.environ.get("DCNV4_LIB") or os.path.join(_HERE, "libdcnv4.so")
 
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_MISALIGNED, ERR_WORKSPACE, ERR_CUDA = range(7)
 _STATUS = {1: "INVALID_ARG", 2: "SHAPE", 3: "UNSUPPORTED", 4: "MISALIGNED", 5: "WORKSPACE",

@@ -142,6 +142,14 @@ static inline unsigned flat_blocks(long long n) {
   return (unsigned)(blocks < 1 ? 1 : blocks);
 }
 
+#ifdef DCNV4_VARIANT_MIN  // A/B variant builds (scripts/build_variant.py): D = 16 only
+#define DCNV4_TABLE(FN, T, ...)                                        \
+  switch (lc.nch * 100 + lc.cpl) {                                     \
+    case 202: return FN<T, 2, 2>(lc, g, __VA_ARGS__);                  \
+    case 402: return FN<T, 4, 2>(lc, g, __VA_ARGS__);                  \
+    default: return cudaErrorInvalidConfiguration;                     \
+  }
+#else
 #define DCNV4_TABLE(FN, T, ...)                                        \
   switch (lc.nch * 100 + lc.cpl) {                                     \
     case 101: return FN<T, 1, 1>(lc, g, __VA_ARGS__);                  \
@@ -156,6 +164,7 @@ static inline unsigned flat_blocks(long long n) {
     case 1604: return FN<T, 16, 4>(lc, g, __VA_ARGS__);                \
     default: return cudaErrorInvalidConfiguration;                     \
   }
+#endif
 
 // One storage type's launchers (used by dcnv4_f32.cu / _f16.cu / _bf16.cu).
 #define DCNV4_DEFINE(SUFFIX, T)                                                                 \

@@ -32,6 +32,15 @@
 
 #include <type_traits>
 
+// Compile-time experiment knobs (scripts/build_variant.py builds A/B libraries with -D;
+// never set in the product build).
+// DCNV4_BWD_ABL: timing-only phase ablation of bwd33 (wrong results): bit 0 skips the P4
+// pull, bit 1 the P3 corner gathers and dots, bit 2 the P1 count, P3 filing and P4 pull,
+// bit 3 the P3 grad_offset_mask stores (profiles/r02_bwd_blockpull_rejected.jsonl).
+#ifndef DCNV4_BWD_ABL
+#define DCNV4_BWD_ABL 0
+#endif
+
 namespace dcnv4 {
 
 // Geometry handed to every kernel by value (validated on the host; per-image element
@@ -1260,7 +1269,8 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
     // DCNv4: one thread per (item, sample) over the whole tile (the L lanes of an item do
     // not repeat each other's coordinate work); DCNv3 softmax: each item's lanes (m needs
     // the softmax over all K of the item).
-    if (!g.softmax && L >= 2) {
+    if (DCNV4_BWD_ABL & 4) {
+    } else if (!g.softmax && L >= 2) {
       const int nsamp = npix * GC * K;
       for (int sidx = tid; sidx < nsamp; sidx += blockDim.x) {
         const int it9 = (sidx * 7282) >> 16;  // sidx / 9 (exact for sidx < 9216)
@@ -1326,6 +1336,7 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
                         make_float2(0.f, 0.f)};
 #pragma unroll
         for (int h = 0; h < CPL; ++h) {
+          if (DCNV4_BWD_ABL & 2) break;
           const uint32_t a0 = hb[h] + off;
           uint4 u[4] = {lds16(a0), lds16(a0 + PB), lds16(a0 + ROWB), lds16(a0 + ROWB + PB)};
 #pragma unroll
@@ -1347,7 +1358,8 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
         }
         gmv[k] = P.in ? sgm : 0.f;
         // d/d dx_k, d/d dy_k (samples beyond the halo are written by the global path below)
-        if (L >= 2) {
+        if (DCNV4_BWD_ABL & 8) {
+        } else if (L >= 2) {
           if (lg < 2 && !(P.fin && !P.in))
             grow[2 * k + lg] = Elem<T>::from_f32(P.in ? s * m[k] * (lg ? sgy : sgx) : 0.f);
         } else if (!(P.fin && !P.in)) {
@@ -1359,7 +1371,7 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
         for (int r = 0; r < QPL; ++r) {
           const int q = (lg % 4) + r * L;
           const float a = m[k] * pick4(w, q);
-          if (lg < 4 && q < 4 && pick4(P.ok, q) && a != 0.f) {
+          if (!(DCNV4_BWD_ABL & 4) && lg < 4 && q < 4 && pick4(P.ok, q) && a != 0.f) {
             const int tt = (P.yl + (q >> 1)) * HWC + P.xl + (q & 1);
             const int e = atomicAdd(&fill[gl * NT + tt], 1);
             if constexpr (ENT8) {
@@ -1450,7 +1462,8 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
           for (int k = 0; k < K; ++k) gmv[k] = m[k] * (gmv[k] - dot);
         }
 #pragma unroll
-        for (int k = 0; k < K; ++k) grow[2 * K + k] = Elem<T>::from_f32(gmv[k]);
+        for (int k = 0; k < K; ++k)
+          if (!(DCNV4_BWD_ABL & 8)) grow[2 * K + k] = Elem<T>::from_f32(gmv[k]);
       }
     }
     // padding channels [3GK, S) of grad_offset_mask: written 0 by the last group run
@@ -1472,7 +1485,8 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
       constexpr int NCL = NCH / PC;  // lanes per (halo pixel, group)
       float* gximg = gx32 + (long long)n * H * W * C;
       long long* gxqimg = gx64 + (long long)n * H * W * C;
-      for (int f = tid; f < NT * GC * NCL; f += blockDim.x) {
+      const int ntask = (DCNV4_BWD_ABL & 5) ? 0 : NT * GC * NCL;
+      for (int f = tid; f < ntask; f += blockDim.x) {
         const int cl = f % NCL;
         const int gg = (f / NCL) % GC;
         const int rk = f / (NCL * GC);

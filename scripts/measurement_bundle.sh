@@ -1,4 +1,4 @@
-# Round-2 measurement bundle: tests, smoke, sanitizer on the new kernels, bench lines,
+# Measurement bundle (run under gpurun from the repo root): tests, smoke, sanitizer on the new kernels, bench lines,
 # reference arm, launch list, ncu of the dominant kernel, CPU baseline protocol.
 set -x
 timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/b_pytest_gpu.txt 2>&1; echo "exit $?" >> gpurun_out/b_pytest_gpu.txt
