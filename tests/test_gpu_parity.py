@@ -147,6 +147,12 @@ CASES = [
     ("halo_G4_pad2", _geom(1, 9, 10, 4, 16, p=(2, 2)), "u2"),
     ("halo_G4_softmax", _geom(2, 10, 9, 4, 16, softmax=True), "u8"),
     ("halo_G4_zero", _geom(2, 10, 9, 4, 16), "zero"),
+    # offset tails over several tiles: the forward's shifted extra halo passes (3x3 boxes
+    # around each tile's halo) and, beyond them, the global gathers
+    ("halo_u8_multi_tile", _geom(1, 30, 27, 4, 16), "u8"),
+    ("halo_u8_scale1.3", _geom(1, 21, 19, 4, 16, scale=1.3), "u8"),
+    ("halo_u8_softmax", _geom(1, 19, 22, 4, 16, softmax=True), "u8"),
+    ("halo_u8_pad0", _geom(1, 20, 18, 4, 16, p=(0, 0)), "u8"),
 ]
 
 
