@@ -1,7 +1,7 @@
 """Per-source-line summary of an ncu report's source page (cuda,sass view): stall samples,
 instructions, shared wavefronts (total / excessive) for the lines that matter.
 
-  python scripts/ncu_lines.py report.ncu-rep [--top 40] [--lines a-b]
+  python scripts/ncu_lines.py report.ncu-rep|report_src.csv.gz [--top 40] [--lines a-b]
 """
 import argparse
 import csv
@@ -15,8 +15,12 @@ def main():
     ap.add_argument("--top", type=int, default=40)
     ap.add_argument("--lines", default="")
     args = ap.parse_args()
-    out = subprocess.run(["ncu", "-i", args.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+    if args.rep.endswith(".csv.gz"):  # exported on the box by scripts/ncu_export.sh
+        import gzip
+        out = gzip.open(args.rep, "rt").read()
+    else:
+        out = subprocess.run(["ncu", "-i", args.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = next(r for r in rows if r and r[0] == "Line No")
     ix = {k: i for i, k in enumerate(hdr)}
