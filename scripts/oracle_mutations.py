@@ -36,7 +36,11 @@ MUTATIONS = [
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="")
+    ap.add_argument("--only", default="", help="run only the mutation with this name")
     args = ap.parse_args()
+    muts = [m for m in MUTATIONS if not args.only or m[0] == args.only]
+    if not muts:
+        raise SystemExit(f"no mutation named {args.only!r}")
     lines = []
     with tempfile.TemporaryDirectory() as tmp:
         for d in ("oracle", "tests", "synth", "paper_2401_06197_b200"):
@@ -46,7 +50,7 @@ def main():
         src = os.path.join(tmp, "oracle", "dcnv4_oracle.c")
         base = open(src).read()
         ok = True
-        for name, a, b in MUTATIONS:
+        for name, a, b in muts:
             if a not in base:
                 lines.append(f"{name}: PATTERN NOT FOUND")
                 ok = False
