@@ -34,6 +34,17 @@
 
 // Compile-time experiment knobs (scripts/build_variant.py builds A/B libraries with -D;
 // never set in the product build).
+// bwd33 P4 pair-loop unroll depth, and two accumulator sets (even / odd entries)
+#ifndef DCNV4_P4_UNROLL
+#define DCNV4_P4_UNROLL 4
+#endif
+#ifndef DCNV4_P4_ACC2
+#define DCNV4_P4_ACC2 0
+#endif
+// bwd33 P1 (count) loop unroll depth
+#ifndef DCNV4_P1_UNROLL
+#define DCNV4_P1_UNROLL 1
+#endif
 // DCNV4_BWD_ABL: timing-only phase ablation of bwd33 (wrong results): bit 0 skips the P4
 // pull, bit 1 the P3 corner gathers and dots, bit 2 the P1 count, P3 filing and P4 pull,
 // bit 3 the P3 grad_offset_mask stores (profiles/r02_bwd_blockpull_rejected.jsonl).
@@ -1272,6 +1283,8 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
     if (DCNV4_BWD_ABL & 4) {
     } else if (!g.softmax && L >= 2) {
       const int nsamp = npix * GC * K;
+      constexpr int P1U = DCNV4_P1_UNROLL;
+#pragma unroll P1U
       for (int sidx = tid; sidx < nsamp; sidx += blockDim.x) {
         const int it9 = (sidx * 7282) >> 16;  // sidx / 9 (exact for sidx < 9216)
         const int k = sidx - it9 * 9;
@@ -1551,7 +1564,13 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
           for (int e = 0; e < PC * E; ++e) acc[e] = 0.f;
           // full pairs (branch-free; unrolled so the entry and gy loads of several pairs
           // are in flight together), then the last pair
-#pragma unroll 4
+#if DCNV4_P4_ACC2
+          float acc2[PC * E];
+#pragma unroll
+          for (int e = 0; e < PC * E; ++e) acc2[e] = 0.f;
+#endif
+          constexpr int P4U = DCNV4_P4_UNROLL;
+#pragma unroll P4U
           for (int q = 0; q < np - 1; ++q) {
             const Dec en = dec(q);
             const T* src0 = gyg + en.s0 * (GC * DG);
@@ -1559,9 +1578,17 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
 #pragma unroll
             for (int h = 0; h < PC; ++h) {
               fma_chunk<T>(acc + h * E, en.a0, *reinterpret_cast<const uint4*>(src0 + cc[h]));
+#if DCNV4_P4_ACC2
+              fma_chunk<T>(acc2 + h * E, en.a1, *reinterpret_cast<const uint4*>(src1 + cc[h]));
+#else
               fma_chunk<T>(acc + h * E, en.a1, *reinterpret_cast<const uint4*>(src1 + cc[h]));
+#endif
             }
           }
+#if DCNV4_P4_ACC2
+#pragma unroll
+          for (int e = 0; e < PC * E; ++e) acc[e] += acc2[e];
+#endif
           {
             const Dec en = dec(np - 1);
             const T* src0 = gyg + en.s0 * (GC * DG);
