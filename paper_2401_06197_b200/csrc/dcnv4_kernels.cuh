@@ -34,9 +34,11 @@
 
 // Compile-time experiment knobs (scripts/build_variant.py builds A/B libraries with -D;
 // never set in the product build).
-// bwd33 P4 pair-loop unroll depth, and two accumulator sets (even / odd entries)
+// bwd33 P4 pair-loop unroll depth (fp32 1, half 2: measured best of 1/2/4/8, c4 step
+// 4651 / 4706 / 4803 / 4966 us, c5 1454 / 1450 / 1463 / 1481 us;
+// profiles/r02_bwd_p4_unroll.jsonl), and two accumulator sets (even / odd entries)
 #ifndef DCNV4_P4_UNROLL
-#define DCNV4_P4_UNROLL 4
+#define DCNV4_P4_UNROLL (sizeof(T) == 4 ? 1 : 2)
 #endif
 #ifndef DCNV4_P4_ACC2
 #define DCNV4_P4_ACC2 0
