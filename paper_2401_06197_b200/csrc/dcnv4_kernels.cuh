@@ -43,6 +43,11 @@
 #ifndef DCNV4_P4_ACC2
 #define DCNV4_P4_ACC2 0
 #endif
+// fwd33 software-pipeline depth (gathers issued DEPTH-1 samples ahead of their FMAs; 2 is
+// best: depth 3 / 4 are 1-4% slower on c4 fp32 and c2/c3 fp16, profiles/r02_fwd_pipe_depth.jsonl)
+#ifndef DCNV4_FWD_PIPE
+#define DCNV4_FWD_PIPE 2
+#endif
 // bwd33 P1 (count) loop unroll depth
 #ifndef DCNV4_P1_UNROLL
 #define DCNV4_P1_UNROLL 1
@@ -823,13 +828,15 @@ __device__ __forceinline__ void fwd33_body(const Src& src) {
 #pragma unroll
           for (int h = 0; h < CPL; ++h) fma_chunk<T>(acc + h * E, F.a[q], F.u[q][h]);
       };
-      // software pipeline: the gathers of point k+1 are issued before the FMAs of k
-      Fetched F0, F1;
-      fetch(0, F0);
+      // software pipeline: the gathers of point k+DEPTH-1 are issued before the FMAs of k
+      constexpr int DEPTH = DCNV4_FWD_PIPE;
+      Fetched F[DEPTH];
+#pragma unroll
+      for (int k = 0; k < DEPTH - 1; ++k) fetch(k, F[k]);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        if (k + 1 < K) fetch(k + 1, (k & 1) ? F0 : F1);
-        accum((k & 1) ? F1 : F0);
+        if (k + DEPTH - 1 < K) fetch(k + DEPTH - 1, F[(k + DEPTH - 1) % DEPTH]);
+        accum(F[k % DEPTH]);
       }
       if (outside) {  // rare: |offset| >= 2 px -- bounds-checked global gathers
         const T* ximg = x + (long long)n * H * W * C;
