@@ -48,6 +48,10 @@
 #ifndef DCNV4_FWD_PIPE
 #define DCNV4_FWD_PIPE 2
 #endif
+// bwd33 P4: 16-B chunks per pull lane (NCH / PC lanes per (halo pixel, group))
+#ifndef DCNV4_P4_PC
+#define DCNV4_P4_PC (NCH >= 2 ? 2 : 1)
+#endif
 // bwd33 P1 (count) loop unroll depth
 #ifndef DCNV4_P1_UNROLL
 #define DCNV4_P1_UNROLL 1
@@ -1503,7 +1507,7 @@ __global__ void __launch_bounds__(sizeof(T) == 4 ? 224 : 256, sizeof(T) == 4 ? 3
     // PC = 2 chunks per lane amortise the entry loads; the chunk order alternates with
     // the halo pixel so an 8-lane phase still touches 8 distinct bank quads
     {
-      constexpr int PC = NCH >= 2 ? 2 : 1;
+      constexpr int PC = DCNV4_P4_PC;
       constexpr int NCL = NCH / PC;  // lanes per (halo pixel, group)
       float* gximg = gx32 + (long long)n * H * W * C;
       long long* gxqimg = gx64 + (long long)n * H * W * C;
